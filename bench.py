@@ -1,0 +1,424 @@
+"""Benchmark: averaged-RHS phase x DOF/s on B200 (BASELINE.json metric).
+
+Workload (default): the C5 throughput point at the largest mesh, refinement
+7 -> 512^2 grid, M = 256 (511 live phases), exact exponentials, fp64,
+seeded synthetic geostrophic state (SURVEY.md 8d planar stand-in for the
+spherical C5 sweep).  One "step" = one averaged-RHS evaluation over all 511
+phases.  metric = P * 3 n^2 * steps / device seconds, summed over replicas.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--level 7] [--M 256] [--no-cpu] [--no-sweep]
+
+Multi-GPU: the path is run as independent replicas (north_star: no
+multi-GPU path); under torchrun every rank times its own replica, the time is
+the max over ranks and value = all ranks' units / that time ("scaling": "weak").
+--impl reference times the oracle port of the reference (oracle/pswe_oracle.py,
+numpy + all host threads) on bounded phase samples of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "averaged-RHS phase×DOF/s (1 GPU, fp64)"
+UNIT = "phase*DOF/s"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def init_dist(ws, backend):
+    import torch.distributed as dist
+    if ws > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return dist
+
+
+def max_over_ranks(value: float, ws: int, device=None) -> float:
+    """Max of a float over ranks (device timing rule); identity for one rank."""
+    if ws == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def alg_bytes(n: int, P: int) -> dict:
+    """Algorithmic bytes for one averaged-RHS evaluation on an n^2 grid."""
+    K = n // 3 + 1
+    Kx = 2 * (n // 3) + 1
+    field = 16 * n * K  # one intermediate field, complex128, n x (n/3+1)
+    return {
+        "B_phase": 352 * n * K,  # survey model: 2 * 16 * (7 + 4) * n * K
+        "B_eval": P * 352 * n * K + 112 * Kx * K,
+        # our passes: A writes 5 fields (+ reads U, b), B reads 5 writes 4, C reads 4
+        "passA_phase": 5 * field + 4 * 16 * Kx * K,
+        "passB_phase": 9 * field,
+        "passC_phase": 4 * field,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, r[3:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flush_l2(buf):
+    buf.add_(1.0)  # 256 MiB write > 126 MB L2
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(case, nodes, threads):
+    """Time the oracle port on a subset of live nodes; returns (seconds, phases)."""
+    from oracle import pswe_oracle as O
+    g, p = case.grid, case.params
+    S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, p.f, p.g, p.H, p.b)
+    U = np.stack([case.state.u, case.state.v, case.state.eta])
+    q = case.quadrature
+    t0 = time.perf_counter()
+    O.averaged_tendency(S, U, q.s, q.w, workers=threads, nodes=nodes)
+    return time.perf_counter() - t0, len(nodes)
+
+
+def cpu_baseline(case, budget_s: float = 12.0, threads: int | None = None) -> dict:
+    """Bounded CPU sample of the same workload: consecutive live nodes until ~budget_s."""
+    threads = threads or cpu_threads()
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    live = [i for i in range(len(case.quadrature.w)) if case.quadrature.w[i] != 0.0]
+    batch = max(1, min(threads, len(live)))
+    used, phases, start = 0.0, 0, 0
+    while used < budget_s and start < len(live):
+        nodes = live[start:start + batch]
+        dt, k = oracle_sample(case, nodes, threads)
+        used += dt
+        phases += k
+        start += batch
+    value = phases * case.dof / used
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle/pswe_oracle.py averaged_tendency on {phases} of {case.P} live phases of "
+                      f"{case.name} ({case.grid.nx}^2), {threads} threads, {used:.1f} s"}
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the oracle port of the reference on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2103_07706_b200 import cases
+    case = cases.case_c5(args.level, args.M)
+    threads = cpu_threads()
+    live = [i for i in range(len(case.quadrature.w)) if case.quadrature.w[i] != 0.0]
+    per_step = max(1, min(len(live), threads))
+    for _ in range(args.warmup):
+        oracle_sample(case, live[:per_step], threads)
+    total, phases = 0.0, 0
+    for k in range(args.steps):
+        start = (k * per_step) % len(live)
+        nodes = (live + live)[start:start + per_step]
+        dt, p = oracle_sample(case, nodes, threads)
+        total += dt
+        phases += p
+    value = phases * case.dof / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded planar C5 stand-in, SURVEY.md 8d)",
+        "config": workload_config(case),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{per_step} of {case.P} live phases per step, oracle/pswe_oracle.py, "
+                                   f"{threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(case):
+    return {"workload": f"C5 averaged RHS, refinement {int(math.log2(case.grid.nx)) - 2} -> "
+                        f"{case.grid.nx}^2 grid, M={case.M} ({case.P} live phases), exact exponentials",
+            "grid": case.grid.nx, "M": case.M, "phases": case.P, "dof": case.dof,
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
+def load_traffic(n):
+    """ncu dram bytes per passB launch from the committed profile summary, if present."""
+    for path in sorted((ROOT / "profiles").glob("ncu_summary_r*.json"), reverse=True):
+        try:
+            d = json.loads(path.read_text())
+            ent = d.get("passB", {}).get(str(n))
+            if ent:
+                return ent
+        except (OSError, ValueError):
+            continue
+    return None
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2103_07706_b200 as pk
+    from paper_2103_07706_b200 import cases
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        init_dist(ws, "nccl")
+    dev = torch.device("cuda", local)
+    case = cases.case_c5(args.level, args.M)
+    n, P = case.grid.nx, case.P
+    ctx = pk.dynamics.context(case.state, case.params)
+    ctx.set_propagator("exact")
+    ctx.set_quadrature(case.quadrature.s, case.quadrature.w)
+    U = pk.dynamics.upload(ctx, case.state)
+    Uc = ctx.pack(U)
+    Ac = ctx.empty_compact()
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        ctx.averaged_tendency_compact(Uc, Ac)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device time of K evaluations, L2 flushed before each
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier(ws)
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush_l2(flush)
+        starts[k].record(stream)
+        ctx.averaged_tendency_compact(Uc, Ac)
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    launches = ctx.launch_count - launches0
+    clocks = sampler.stop()
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    dev_ms = max_over_ranks(dev_ms, ws, dev)
+    ms_per_step = dev_ms / args.steps
+    units = ws * P * case.dof * args.steps
+    value = units / (dev_ms * 1e-3)
+
+    # ---- per-kernel split (CUDA events around each launch, separate pass)
+    ctx.profile(True)
+    for _ in range(args.steps):
+        flush_l2(flush)
+        ctx.averaged_tendency_compact(Uc, Ac)
+    torch.cuda.synchronize()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ab = alg_bytes(n, P)
+    peak = peak_hbm()
+    kern = {}
+    for name in ("passA", "passB", "passC", "reduce"):
+        ms, cnt = prof[name]
+        kern[name] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
+                      "share": None}
+    tot = sum(v["ms_per_step"] for v in kern.values()) or 1.0
+    for v in kern.values():
+        v["share"] = v["ms_per_step"] / tot
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
+    per_launch_ms = prof[dom][0] / max(prof[dom][1], 1)
+    phases_per_launch = P / max(kern[dom]["launches_per_step"], 1e-9)
+    dom_bytes = ab[f"{dom}_phase"] * phases_per_launch if dom.startswith("pass") else 3 * 16 * n * n
+    achieved = dom_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = load_traffic(n)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak["value"],
+                "unit": "GB/s", "frac": achieved / peak["value"], "peak_source": peak["source"],
+                "traffic": traffic, "alg_bytes_per_launch": dom_bytes,
+                "launch_ms": per_launch_ms}
+    rhs_achieved = ab["B_eval"] / (ms_per_step * 1e-3) / 1e9
+    rhs_roofline = {"bound": "hbm", "B_eval": ab["B_eval"], "achieved": rhs_achieved,
+                    "peak": peak["value"], "unit": "GB/s", "frac": rhs_achieved / peak["value"],
+                    "note": "SURVEY.md 8d algorithmic bytes of one whole averaged-RHS evaluation"}
+
+    # ---- end to end through the public drop-in API, host numpy in/out
+    e2e = None
+    if not args.no_e2e:
+        pk.averaged_tendency(case.state, case.quadrature, case.params, pk.PropagatorSpec.exact())
+        torch.cuda.synchronize()
+        barrier(ws)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            out = pk.averaged_tendency(case.state, case.quadrature, case.params, pk.PropagatorSpec.exact())
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
+        e2e = {"value": ws * P * case.dof * args.e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": 3 * 16 * n * n, "d2h_bytes_per_step": 3 * 16 * n * n,
+               "ms_per_step": 1e3 * e2e_s / args.e2e_steps,
+               "path": "paper_2103_07706_b200.averaged_tendency(numpy State) -> C ABI -> numpy State"}
+        del out
+
+    sweep = None
+    if not args.no_sweep and rank == 0:
+        sweep = run_sweep(pk, cases, torch, flush, stream)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(case, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded planar C5 stand-in, SURVEY.md 8d)",
+            "config": workload_config(case) | {"parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+            "roofline": roofline, "rhs_roofline": rhs_roofline, "kernels": kern,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "gpu": torch.cuda.get_device_name(local), "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_sweep(pk, cases, torch, flush, stream, steps=3):
+    """GPU-only phase x DOF/s for the other C5 points (refinement 4-7 x M)."""
+    out = []
+    for r in (4, 5, 6, 7):
+        for M in (8, 32, 128, 256):
+            c = cases.case_c5(r, M)
+            ctx = pk.dynamics.context(c.state, c.params)
+            ctx.set_propagator("exact")
+            ctx.set_quadrature(c.quadrature.s, c.quadrature.w)
+            Uc = ctx.pack(pk.dynamics.upload(ctx, c.state))
+            Ac = ctx.empty_compact()
+            ctx.averaged_tendency_compact(Uc, Ac)
+            ms = 0.0
+            for _ in range(steps):
+                flush_l2(flush)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                ctx.averaged_tendency_compact(Uc, Ac)
+                b.record(stream)
+                torch.cuda.synchronize()
+                ms += a.elapsed_time(b)
+            ms /= steps
+            ab = alg_bytes(c.grid.nx, c.P)
+            out.append({"n": c.grid.nx, "M": M, "P": c.P, "ms": ms,
+                        "phase_dof_per_s": c.P * c.dof / (ms * 1e-3),
+                        "alg_GBps": ab["B_eval"] / (ms * 1e-3) / 1e9})
+    return out
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return {"value": float(json.loads(p.read_text())["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except (OSError, ValueError, KeyError):
+        return {"value": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--level", type=int, default=7)
+    ap.add_argument("--M", type=int, default=256)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
+        args.warmup = 3
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

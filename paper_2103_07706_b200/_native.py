@@ -1,0 +1,301 @@
+"""ctypes binding of ``libpswe_b200.so`` (declared in ``include/pswe_b200.h``).
+
+PyTorch is used only as the device-memory / stream plumbing: tensors are
+allocated with torch, their raw pointers and torch's current CUDA stream are
+handed to the C ABI.  There is no CPU fallback: if the library or a CUDA
+device is missing every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+import threading
+
+import numpy as np
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "lib" / "libpswe_b200.so"
+
+PSWE_OK = 0
+PSWE_EINVAL = 1
+PSWE_ECUDA = 2
+PSWE_EUNSUPPORTED = 3
+PSWE_ENONFINITE = 4
+PSWE_ESTATE = 5
+
+_lib = None
+_lib_lock = threading.Lock()
+
+_c_int_p = ctypes.POINTER(ctypes.c_int)
+_vp = ctypes.c_void_p
+_d = ctypes.c_double
+_i = ctypes.c_int
+
+# name -> (restype, argtypes); the ABI exported by include/pswe_b200.h
+SIGNATURES = {
+    "pswe_version": (_i, []),
+    "pswe_last_error": (ctypes.c_char_p, []),
+    "pswe_create": (_i, [ctypes.POINTER(_vp), _i, _i, _d, _d, _d, _d, _d, _i]),
+    "pswe_destroy": (None, [_vp]),
+    "pswe_set_topography": (_i, [_vp, _vp, _vp]),
+    "pswe_set_quadrature": (_i, [_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_d)]),
+    "pswe_set_propagator": (_i, [_vp, _i, _d, _i, ctypes.POINTER(_d)]),
+    "pswe_compact_shape": (_i, [_vp, _c_int_p, _c_int_p]),
+    "pswe_pack": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pswe_unpack": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pswe_averaged_tendency_compact": (_i, [_vp, _vp, _vp, _vp]),
+    "pswe_averaged_tendency": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pswe_apply_nonlinear": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pswe_apply_linear": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pswe_propagate": (_i, [_vp, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pswe_ssprk3_step": (_i, [_vp, _d, _vp, _vp, _vp, _vp, _vp, _vp, _c_int_p, _c_int_p, _vp]),
+    "pswe_run": (_i, [_vp, _d, _i, _vp, _vp, _vp, _c_int_p, _c_int_p, _c_int_p, _vp]),
+    "pswe_max_frequency": (_d, [_vp]),
+    "pswe_launch_count": (ctypes.c_int64, [_vp]),
+    "pswe_set_chunk_bytes": (_i, [_vp, ctypes.c_size_t]),
+    "pswe_profile_enable": (_i, [_vp, _i]),
+    "pswe_profile_read": (_i, [_vp, ctypes.POINTER(_d), ctypes.POINTER(ctypes.c_int64), _i]),
+}
+
+KERNEL_CLASSES = ("passA", "passB", "passC", "reduce", "pack", "unpack", "stage")
+
+
+class NativeError(RuntimeError):
+    """A failed C-ABI call; ``code`` is the PSWE_* status."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def load_library(path: os.PathLike | None = None):
+    """Load and declare the shared library (no CUDA work happens here)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = pathlib.Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"B200 extension {p} is missing; build it with `make` or "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def _check(rc: int) -> None:
+    if rc != PSWE_OK:
+        msg = _lib.pswe_last_error().decode("utf-8", "replace")
+        if rc in (PSWE_EINVAL, PSWE_EUNSUPPORTED):
+            err = ValueError(msg)
+            err.code = rc
+            raise err
+        raise NativeError(rc, msg)
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2103_07706_b200 needs a CUDA device (sm_100a); "
+                           "the B200 path has no CPU fallback")
+    return torch
+
+
+def _dptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(torch):
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Context:
+    """One grid + physics on one CUDA device (``pswe_ctx``).
+
+    Holds the last quadrature / propagator / topography pushed to the
+    library so repeated calls with the same objects cost nothing.
+    """
+
+    def __init__(self, nx: int, ny: int, Lx: float, Ly: float, f: float, g: float, H: float,
+                 device: int | None = None):
+        torch = _torch()
+        load_library()
+        self.torch = torch
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.nx, self.ny = int(nx), int(ny)
+        h = ctypes.c_void_p()
+        _check(_lib.pswe_create(ctypes.byref(h), self.nx, self.ny, float(Lx), float(Ly),
+                                float(f), float(g), float(H), self.device))
+        self.h = h
+        ky, kx = ctypes.c_int(), ctypes.c_int()
+        _check(_lib.pswe_compact_shape(h, ctypes.byref(ky), ctypes.byref(kx)))
+        self.Ky, self.Kx = ky.value, kx.value
+        self._quad_key = None
+        self._prop_key = None
+        self._b_obj = None
+        self._b_copy = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None:
+            _lib.pswe_destroy(h)
+            self.h = None
+
+    # ---- configuration -------------------------------------------------
+    @property
+    def max_frequency(self) -> float:
+        return float(_lib.pswe_max_frequency(self.h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(_lib.pswe_launch_count(self.h))
+
+    def profile(self, enable: bool) -> None:
+        _check(_lib.pswe_profile_enable(self.h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{class: (milliseconds, launches)} since the last read."""
+        n = len(KERNEL_CLASSES)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        _check(_lib.pswe_profile_read(self.h, ms, cnt, n))
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES)}
+
+    def set_chunk_bytes(self, nbytes: int) -> None:
+        _check(_lib.pswe_set_chunk_bytes(self.h, int(nbytes)))
+
+    def set_quadrature(self, s: np.ndarray, w: np.ndarray) -> None:
+        s = np.ascontiguousarray(s, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        key = (s.tobytes(), w.tobytes())
+        if key == self._quad_key:
+            return
+        dp = ctypes.POINTER(ctypes.c_double)
+        _check(_lib.pswe_set_quadrature(self.h, len(s), s.ctypes.data_as(dp), w.ctypes.data_as(dp)))
+        self._quad_key = key
+
+    def set_propagator(self, kind: str, Lambda: float = 0.0, n_poly: int = 1,
+                       a: np.ndarray | None = None) -> None:
+        key = (kind, float(Lambda), int(n_poly))
+        if key == self._prop_key:
+            return
+        if kind == "exact":
+            _check(_lib.pswe_set_propagator(self.h, 0, 0.0, 1, None))
+        elif kind == "chebyshev":
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            _check(_lib.pswe_set_propagator(self.h, 1, float(Lambda), int(n_poly),
+                                            a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        else:
+            raise ValueError(f"unknown propagator kind {kind!r}")
+        self._prop_key = key
+
+    def set_topography(self, b) -> None:
+        """Upload b (full spectral layout) unless this exact content is already set."""
+        if b is self._b_obj:
+            return
+        arr = np.asarray(b, dtype=np.complex128)
+        if self._b_copy is not None and self._b_copy.shape == arr.shape and np.array_equal(self._b_copy, arr):
+            self._b_obj = b
+            return
+        bt = self.to_device(arr)
+        _check(_lib.pswe_set_topography(self.h, _dptr(bt), _stream(self.torch)))
+        self.torch.cuda.current_stream().synchronize()
+        self._b_obj = b
+        self._b_copy = arr.copy()
+
+    # ---- tensors ---------------------------------------------------------
+    def to_device(self, arr):
+        """numpy (nx, ny) complex128 -> contiguous CUDA tensor."""
+        torch = self.torch
+        if isinstance(arr, torch.Tensor):
+            return arr.to(device=f"cuda:{self.device}", dtype=torch.complex128).contiguous()
+        a = np.ascontiguousarray(arr, dtype=np.complex128)
+        return torch.from_numpy(a).to(device=f"cuda:{self.device}", non_blocking=False)
+
+    def empty_full(self):
+        return self.torch.empty((self.nx, self.ny), dtype=self.torch.complex128,
+                                device=f"cuda:{self.device}")
+
+    def empty_compact(self):
+        return self.torch.empty((3, self.Ky, self.Kx), dtype=self.torch.complex128,
+                                device=f"cuda:{self.device}")
+
+    # ---- operators (device tensors in/out) ---------------------------------
+    def _call3(self, fn, U, *extra):
+        out = [self.empty_full() for _ in range(3)]
+        _check(fn(self.h, *extra, *(_dptr(x) for x in U), *(_dptr(x) for x in out),
+                  _stream(self.torch)))
+        return out
+
+    def averaged_tendency(self, U):
+        return self._call3(_lib.pswe_averaged_tendency, U)
+
+    def averaged_tendency_compact(self, Uc, out=None):
+        out = self.empty_compact() if out is None else out
+        _check(_lib.pswe_averaged_tendency_compact(self.h, _dptr(Uc), _dptr(out), _stream(self.torch)))
+        return out
+
+    def pack(self, U, out=None):
+        out = self.empty_compact() if out is None else out
+        _check(_lib.pswe_pack(self.h, *(_dptr(x) for x in U), _dptr(out), _stream(self.torch)))
+        return out
+
+    def unpack(self, Uc):
+        out = [self.empty_full() for _ in range(3)]
+        _check(_lib.pswe_unpack(self.h, _dptr(Uc), *(_dptr(x) for x in out), _stream(self.torch)))
+        return out
+
+    def apply_nonlinear(self, U):
+        return self._call3(_lib.pswe_apply_nonlinear, U)
+
+    def apply_linear(self, U):
+        return self._call3(_lib.pswe_apply_linear, U)
+
+    def propagate(self, t: float, U):
+        return self._call3(_lib.pswe_propagate, U, ctypes.c_double(float(t)))
+
+    def ssprk3_step(self, dt: float, U):
+        """Returns (out, (stage, field)); stage 0 means all stages finite."""
+        out = [self.empty_full() for _ in range(3)]
+        st, fl = ctypes.c_int(0), ctypes.c_int(-1)
+        rc = _lib.pswe_ssprk3_step(self.h, float(dt), *(_dptr(x) for x in U),
+                                   *(_dptr(x) for x in out), ctypes.byref(st), ctypes.byref(fl),
+                                   _stream(self.torch))
+        if rc == PSWE_ENONFINITE:
+            return out, (st.value, fl.value)
+        _check(rc)
+        return out, (0, -1)
+
+    def run(self, dt: float, nsteps: int, U):
+        """In-place nsteps on U (list of 3 tensors). Returns (bad_step, stage, field)."""
+        bs, st, fl = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(-1)
+        rc = _lib.pswe_run(self.h, float(dt), int(nsteps), *(_dptr(x) for x in U),
+                           ctypes.byref(bs), ctypes.byref(st), ctypes.byref(fl), _stream(self.torch))
+        if rc == PSWE_ENONFINITE:
+            return bs.value, st.value, fl.value
+        _check(rc)
+        return 0, 0, -1
+
+
+_ctx_cache: dict = {}
+_ctx_lock = threading.Lock()
+
+
+def context_for(nx, ny, Lx, Ly, f, g, H) -> Context:
+    """Cached context per (grid, physics constants, device)."""
+    torch = _torch()
+    key = (int(nx), int(ny), float(Lx), float(Ly), float(f), float(g), float(H),
+           torch.cuda.current_device(), threading.get_ident())
+    with _ctx_lock:
+        ctx = _ctx_cache.get(key)
+        if ctx is None:
+            ctx = Context(nx, ny, Lx, Ly, f, g, H)
+            _ctx_cache[key] = ctx
+        return ctx

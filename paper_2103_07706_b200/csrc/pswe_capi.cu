@@ -1,0 +1,702 @@
+// C ABI + host orchestration for the B200 phase-averaged RHS (see
+// include/pswe_b200.h).  One context = one grid/physics on one device; it
+// owns the constant tables, the chunk intermediates and the stepper scratch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pswe_b200.h"
+#include "pswe_kernels.cuh"
+
+using namespace pswe;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return set_err(PSWE_ECUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_),      \
+                     __FILE__, __LINE__, #call);                                             \
+  } while (0)
+
+#define TRY(call)              \
+  do {                         \
+    int rc_ = (call);          \
+    if (rc_ != PSWE_OK) return rc_; \
+  } while (0)
+
+bool pow2_ok(int n) { return n >= 8 && n <= 1024 && (n & (n - 1)) == 0; }
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int alloc(size_t count) {
+    if (count <= n) return PSWE_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    CU(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    n = count;
+    return PSWE_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct pswe_ctx {
+  int device = 0;
+  int nx = 0, ny = 0, kxm = 0, kym = 0, Kx = 0, Ky = 0;
+  double Lx = 0, Ly = 0, f = 0, g = 0, H = 0;
+  double lam_max = 0;
+  std::vector<double> kx_full, ky_full;
+  DevBuf<double> kxc, kyc, kxf, kyf;
+  DevBuf<double2> twx, twy, bc;
+  // quadrature (live nodes only)
+  std::vector<double> s_live, w_live;
+  std::vector<int> k_live;
+  int M = 0;
+  bool quad_set = false;
+  DevBuf<double> s_dev, w_dev;
+  DevBuf<double> zero_s, one_w;  // single node s=0, w=1 for apply_nonlinear
+  // propagator
+  int kind = 0, n_poly = 1;
+  double Lambda = 0;
+  DevBuf<double> a_dev;
+  // scratch
+  size_t chunk_bytes = size_t(40) << 20;
+  DevBuf<double2> inter, slots, Uc, Ac, Ac2;
+  DevBuf<double2> full_tmp;  // stepper: edt, u1, u2 (3 states) + run ping-pong (2 states)
+  DevBuf<int> flags;
+  int* flags_host = nullptr;
+  int64_t launches = 0;
+  // per-kernel event profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  size_t ev_used = 0;
+
+  GridDev grid() const {
+    GridDev G;
+    G.nx = nx; G.ny = ny; G.kxm = kxm; G.kym = kym; G.Kx = Kx; G.Ky = Ky;
+    G.ph = Phys{f, g, H};
+    G.inv_n2 = 1.0 / ((double)nx * (double)ny);
+    G.kxc = kxc.p; G.kyc = kyc.p; G.kxf = kxf.p; G.kyf = kyf.p;
+    G.twx = twx.p; G.twy = twy.p; G.bc = bc.p;
+    return G;
+  }
+  Prop prop() const { return Prop{kind, n_poly, Lambda, a_dev.p}; }
+  size_t compact_elems() const { return (size_t)3 * Ky * Kx; }
+  size_t full_elems() const { return (size_t)nx * ny; }
+};
+
+namespace {
+
+int elem_grid(size_t n) {
+  size_t b = (n + 255) / 256;
+  return (int)std::max<size_t>(1, std::min<size_t>(b, 148 * 16));
+}
+
+// optional per-launch event bracketing: PROF_BEGIN before a launch, PROF_END after
+cudaEvent_t next_event(pswe_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+struct ProfScope {
+  pswe_ctx* c;
+  int cls;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(pswe_ctx* c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
+    if (c->prof) {
+      a = next_event(c);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (c->prof) {
+      cudaEvent_t b = next_event(c);
+      cudaEventRecord(b, st);
+      c->recs.push_back({cls, a, b});
+    }
+  }
+};
+
+// ---------------------------------------------------------------- dispatch
+template <int N>
+constexpr int groups_per_cta() {
+  return (1024 / N) > 0 ? (1024 / N) : 1;
+}
+
+template <int NX>
+int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, cudaStream_t st) {
+  constexpr int GPC = groups_per_cta<NX>();
+  const int tasks = np * c->Ky;
+  const int blocks = (tasks + GPC - 1) / GPC;
+  ProfScope ps(c, 0, st);
+  passA_kernel<NX, GPC><<<blocks, GPC * NX / 8, 0, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->inter.p);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+template <int NY>
+int launchB(pswe_ctx* c, int np, cudaStream_t st) {
+  constexpr int G = groups_per_cta<NY>();
+  const size_t smem = ((size_t)5 * c->Ky * G + (size_t)G * FFTSize<NY>::PAD) * sizeof(double2);
+  auto kern = passB_kernel<NY, G>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int tasks = np * c->nx;
+  const int blocks = (tasks + G - 1) / G;
+  ProfScope ps(c, 1, st);
+  kern<<<blocks, G * NY / 8, smem, st>>>(c->grid(), np, c->inter.p);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+template <int NX>
+int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, cudaStream_t st) {
+  constexpr int GPC = groups_per_cta<NX>();
+  const size_t smem = (size_t)GPC * (FFTSize<NX>::PAD + 7 * c->Kx) * sizeof(double2);
+  auto kern = passC_kernel<NX, GPC>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int tasks = c->Ky * Gc;
+  const int blocks = (tasks + GPC - 1) / GPC;
+  ProfScope ps(c, 2, st);
+  kern<<<blocks, GPC * NX / 8, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, c->inter.p, c->slots.p, first);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, cudaStream_t st) {
+  switch (c->nx) {
+    case 8: return launchA<8>(c, ph, p0, np, Uc, st);
+    case 16: return launchA<16>(c, ph, p0, np, Uc, st);
+    case 32: return launchA<32>(c, ph, p0, np, Uc, st);
+    case 64: return launchA<64>(c, ph, p0, np, Uc, st);
+    case 128: return launchA<128>(c, ph, p0, np, Uc, st);
+    case 256: return launchA<256>(c, ph, p0, np, Uc, st);
+    case 512: return launchA<512>(c, ph, p0, np, Uc, st);
+    case 1024: return launchA<1024>(c, ph, p0, np, Uc, st);
+  }
+  return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
+}
+int dispatchB(pswe_ctx* c, int np, cudaStream_t st) {
+  switch (c->ny) {
+    case 8: return launchB<8>(c, np, st);
+    case 16: return launchB<16>(c, np, st);
+    case 32: return launchB<32>(c, np, st);
+    case 64: return launchB<64>(c, np, st);
+    case 128: return launchB<128>(c, np, st);
+    case 256: return launchB<256>(c, np, st);
+    case 512: return launchB<512>(c, np, st);
+    case 1024: return launchB<1024>(c, np, st);
+  }
+  return set_err(PSWE_EUNSUPPORTED, "unsupported ny = %d", c->ny);
+}
+int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, cudaStream_t st) {
+  switch (c->nx) {
+    case 8: return launchC<8>(c, ph, p0, np, Gc, first, st);
+    case 16: return launchC<16>(c, ph, p0, np, Gc, first, st);
+    case 32: return launchC<32>(c, ph, p0, np, Gc, first, st);
+    case 64: return launchC<64>(c, ph, p0, np, Gc, first, st);
+    case 128: return launchC<128>(c, ph, p0, np, Gc, first, st);
+    case 256: return launchC<256>(c, ph, p0, np, Gc, first, st);
+    case 512: return launchC<512>(c, ph, p0, np, Gc, first, st);
+    case 1024: return launchC<1024>(c, ph, p0, np, Gc, first, st);
+  }
+  return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
+}
+
+// Averaged RHS on compact data: chunks of phases through passes A, B, C,
+// then the ordered slot reduction.  `P` live phases in (s, w) device arrays.
+int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const double2* Uc, double2* Ac,
+                cudaStream_t st) {
+  const size_t per_phase = (size_t)5 * c->Ky * c->nx;  // double2 elements
+  int CP = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
+  CP = std::min(CP, P);
+  const int target_groups = 2 * 148;
+  int Gc = std::max(1, (target_groups + c->Ky - 1) / c->Ky);
+  Gc = std::min(Gc, CP);
+  TRY(c->inter.alloc(per_phase * CP));
+  TRY(c->slots.alloc((size_t)Gc * c->compact_elems()));
+  PhaseDev ph{s, w, P};
+  for (int p0 = 0; p0 < P; p0 += CP) {
+    const int np = std::min(CP, P - p0);
+    TRY(dispatchA(c, ph, p0, np, Uc, st));
+    TRY(dispatchB(c, np, st));
+    TRY(dispatchC(c, ph, p0, np, Gc, p0 == 0 ? 1 : 0, st));
+  }
+  const size_t n = c->compact_elems();
+  ProfScope ps(c, 3, st);
+  reduce_slots_kernel<<<elem_grid(n), 256, 0, st>>>(c->slots.p, Gc, n, Ac);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+int check_cheb(const pswe_ctx* c, double t, std::string* msg) {
+  if (c->kind != 1 || t == 0.0) return PSWE_OK;
+  const double need = std::fabs(t) * c->lam_max;
+  if (need > c->Lambda * (1.0 + 1e-9)) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "|t| * max_frequency = %.6g exceeds Lambda = %.6g; enlarge Lambda or shorten t",
+             need, c->Lambda);
+    *msg = buf;
+    return PSWE_EINVAL;
+  }
+  return PSWE_OK;
+}
+
+// host-side Chebyshev precondition over the live nodes, first failure in
+// ascending order wrapped like averaging.py:138-141
+int check_nodes(const pswe_ctx* c) {
+  std::string msg;
+  for (size_t i = 0; i < c->s_live.size(); ++i) {
+    if (check_cheb(c, c->s_live[i], &msg) != PSWE_OK)
+      return set_err(PSWE_EINVAL, "averaging node k = %d (s = %.6g s) failed: %s", c->k_live[i], c->s_live[i],
+                     msg.c_str());
+  }
+  return PSWE_OK;
+}
+
+GridDev grid_of(const pswe_ctx* c) { return c->grid(); }
+
+int ensure_compact(pswe_ctx* c) {
+  TRY(c->Uc.alloc(c->compact_elems()));
+  TRY(c->Ac.alloc(c->compact_elems()));
+  return PSWE_OK;
+}
+
+Full3 f3(const double* u, const double* v, const double* e) {
+  return Full3{(const double2*)u, (const double2*)v, (const double2*)e};
+}
+Full3w f3w(double* u, double* v, double* e) { return Full3w{(double2*)u, (double2*)v, (double2*)e}; }
+Full3 f3c(const Full3w& a) { return Full3{a.u, a.v, a.e}; }
+
+int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
+  const size_t n = c->full_elems();
+  TRY(ensure_compact(c));
+  TRY(c->full_tmp.alloc(n * 15));
+  Full3w edt{c->full_tmp.p, c->full_tmp.p + n, c->full_tmp.p + 2 * n};
+  Full3w u1{c->full_tmp.p + 3 * n, c->full_tmp.p + 4 * n, c->full_tmp.p + 5 * n};
+  Full3w u2{c->full_tmp.p + 6 * n, c->full_tmp.p + 7 * n, c->full_tmp.p + 8 * n};
+  const GridDev G = c->grid();
+  const Prop pr = c->prop();
+  const int P = (int)c->s_live.size();
+  const int gb = elem_grid(n);
+  // stage 1
+  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, U.u, U.v, U.e, c->Uc.p);
+  c->launches++;
+  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
+  stage1_kernel<<<gb, 256, 0, st>>>(G, pr, dt, U, c->Ac.p, edt, u1, c->flags.p);
+  c->launches++;
+  // stage 2
+  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, u1.u, u1.v, u1.e, c->Uc.p);
+  c->launches++;
+  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
+  stage2_kernel<<<gb, 256, 0, st>>>(G, pr, dt, U, f3c(u1), c->Ac.p, u2, c->flags.p);
+  c->launches++;
+  // stage 3
+  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, u2.u, u2.v, u2.e, c->Uc.p);
+  c->launches++;
+  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
+  stage3_kernel<<<gb, 256, 0, st>>>(G, pr, dt, f3c(edt), f3c(u2), c->Ac.p, out, c->flags.p);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+int decode_flags(int bits, int* stage, int* field) {
+  for (int st = 1; st <= 3; ++st)
+    for (int fl = 0; fl < 3; ++fl)
+      if (bits & (1 << (3 * (st - 1) + fl))) {
+        *stage = st;
+        *field = fl;
+        return 1;
+      }
+  return 0;
+}
+
+const char* field_name(int f) { return f == 0 ? "u" : (f == 1 ? "v" : "eta"); }
+
+}  // namespace
+
+// =============================================================== C ABI
+extern "C" {
+
+int pswe_version(void) { return 100; }
+
+const char* pswe_last_error(void) { return g_err.c_str(); }
+
+int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, double g, double H, int device) {
+  if (!out) return set_err(PSWE_EINVAL, "null context pointer");
+  *out = nullptr;
+  if (nx < 8 || nx % 2 != 0) return set_err(PSWE_EINVAL, "nx must be even and >= 8, got %d", nx);
+  if (ny < 8 || ny % 2 != 0) return set_err(PSWE_EINVAL, "ny must be even and >= 8, got %d", ny);
+  if (!(Lx > 0)) return set_err(PSWE_EINVAL, "Lx must be positive, got %g", Lx);
+  if (!(Ly > 0)) return set_err(PSWE_EINVAL, "Ly must be positive, got %g", Ly);
+  if (!(g > 0)) return set_err(PSWE_EINVAL, "g must be positive, got %g", g);
+  if (!(H > 0)) return set_err(PSWE_EINVAL, "H must be positive, got %g", H);
+  if (!pow2_ok(nx) || !pow2_ok(ny))
+    return set_err(PSWE_EUNSUPPORTED,
+                   "grid %dx%d not supported by the B200 path (nx, ny must be powers of two in [8, 1024])", nx, ny);
+  CU(cudaSetDevice(device));
+  pswe_ctx* c = new pswe_ctx();
+  c->device = device;
+  c->nx = nx; c->ny = ny; c->Lx = Lx; c->Ly = Ly; c->f = f; c->g = g; c->H = H;
+  c->kxm = nx / 3; c->kym = ny / 3;
+  c->Kx = 2 * c->kxm + 1; c->Ky = c->kym + 1;
+  // wavenumbers exactly as make_grid: 2 pi * wrap / L (grid.py:98-101)
+  c->kx_full.resize(nx);
+  c->ky_full.resize(ny);
+  for (int i = 0; i < nx; ++i) {
+    const int w = i < nx / 2 ? i : i - nx;
+    c->kx_full[i] = 2.0 * M_PI * (double)w / Lx;
+  }
+  for (int j = 0; j < ny; ++j) {
+    const int w = j < ny / 2 ? j : j - ny;
+    c->ky_full[j] = 2.0 * M_PI * (double)w / Ly;
+  }
+  std::vector<double> kxc(c->Kx), kyc(c->Ky);
+  for (int r = 0; r < c->Kx; ++r) {
+    const int w = r <= c->kxm ? r : r - c->Kx;
+    kxc[r] = c->kx_full[(w + nx) % nx];
+  }
+  for (int j = 0; j < c->Ky; ++j) kyc[j] = c->ky_full[j];
+  // max_frequency (dynamics.py:189-192): max over the full grid
+  double lm = 0;
+  for (int i = 0; i < nx; ++i)
+    for (int j = 0; j < ny; ++j) {
+      const double kx = c->kx_full[i], ky = c->ky_full[j];
+      lm = std::max(lm, std::sqrt(f * f + g * H * (kx * kx + ky * ky)));
+    }
+  c->lam_max = lm;
+  int rc = PSWE_OK;
+  auto up = [&](DevBuf<double>& b, const std::vector<double>& h) -> int {
+    TRY(b.alloc(h.size()));
+    CU(cudaMemcpy(b.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return PSWE_OK;
+  };
+  if ((rc = up(c->kxc, kxc)) || (rc = up(c->kyc, kyc)) || (rc = up(c->kxf, c->kx_full)) ||
+      (rc = up(c->kyf, c->ky_full))) {
+    pswe_destroy(c);
+    return rc;
+  }
+  if ((rc = c->twx.alloc(nx)) || (rc = c->twy.alloc(ny)) || (rc = c->bc.alloc((size_t)c->Ky * c->Kx)) ||
+      (rc = c->flags.alloc(1))) {
+    pswe_destroy(c);
+    return rc;
+  }
+  twiddle_kernel<<<(nx + 255) / 256, 256>>>(c->twx.p, nx);
+  twiddle_kernel<<<(ny + 255) / 256, 256>>>(c->twy.p, ny);
+  cudaMemset(c->bc.p, 0, (size_t)c->Ky * c->Kx * sizeof(double2));
+  cudaMemset(c->flags.p, 0, sizeof(int));
+  {
+    std::vector<double> z(1, 0.0), o(1, 1.0);
+    if ((rc = up(c->zero_s, z)) || (rc = up(c->one_w, o))) {
+      pswe_destroy(c);
+      return rc;
+    }
+  }
+  if (cudaMallocHost(&c->flags_host, sizeof(int)) != cudaSuccess) {
+    pswe_destroy(c);
+    return set_err(PSWE_ECUDA, "cudaMallocHost failed");
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    pswe_destroy(c);
+    return set_err(PSWE_ECUDA, "CUDA error %s during context setup", cudaGetErrorString(e));
+  }
+  *out = c;
+  return PSWE_OK;
+}
+
+void pswe_destroy(pswe_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (DevBuf<double>* b : {&c->kxc, &c->kyc, &c->kxf, &c->kyf, &c->s_dev, &c->w_dev, &c->zero_s, &c->one_w, &c->a_dev})
+    b->release();
+  for (DevBuf<double2>* b : {&c->twx, &c->twy, &c->bc, &c->inter, &c->slots, &c->Uc, &c->Ac, &c->Ac2, &c->full_tmp})
+    b->release();
+  c->flags.release();
+  if (c->flags_host) cudaFreeHost(c->flags_host);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
+
+int pswe_set_topography(pswe_ctx* c, const double* b_dev, void* stream) {
+  if (!c || !b_dev) return set_err(PSWE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaSetDevice(c->device));
+  // compact, Hermitian-projected band of b; pack_kernel fills 3 fields, use scratch
+  TRY(c->Uc.alloc(c->compact_elems()));
+  const GridDev G = c->grid();
+  const double2* b = (const double2*)b_dev;
+  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p);
+  c->launches++;
+  CU(cudaMemcpyAsync(c->bc.p, c->Uc.p, (size_t)c->Ky * c->Kx * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+int pswe_set_quadrature(pswe_ctx* c, int n_nodes, const double* s, const double* w) {
+  if (!c || !s || !w) return set_err(PSWE_EINVAL, "null argument");
+  if (n_nodes < 1 || n_nodes % 2 != 1) return set_err(PSWE_EINVAL, "need an odd number of nodes (2M+1), got %d", n_nodes);
+  CU(cudaSetDevice(c->device));
+  c->M = (n_nodes - 1) / 2;
+  c->s_live.clear();
+  c->w_live.clear();
+  c->k_live.clear();
+  for (int i = 0; i < n_nodes; ++i) {
+    if (w[i] != 0.0) {
+      c->s_live.push_back(s[i]);
+      c->w_live.push_back(w[i]);
+      c->k_live.push_back(i - c->M);
+    }
+  }
+  if (c->s_live.empty()) return set_err(PSWE_EINVAL, "quadrature has no node with nonzero weight");
+  const size_t P = c->s_live.size();
+  TRY(c->s_dev.alloc(P));
+  TRY(c->w_dev.alloc(P));
+  CU(cudaMemcpy(c->s_dev.p, c->s_live.data(), P * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(c->w_dev.p, c->w_live.data(), P * sizeof(double), cudaMemcpyHostToDevice));
+  c->quad_set = true;
+  return PSWE_OK;
+}
+
+int pswe_set_propagator(pswe_ctx* c, int kind, double Lambda, int n_poly, const double* a) {
+  if (!c) return set_err(PSWE_EINVAL, "null context");
+  if (kind != 0 && kind != 1) return set_err(PSWE_EINVAL, "unknown propagator kind %d", kind);
+  CU(cudaSetDevice(c->device));
+  if (kind == 1) {
+    if (!(Lambda >= 0)) return set_err(PSWE_EINVAL, "Lambda must be nonnegative, got %g", Lambda);
+    if (n_poly < 1) return set_err(PSWE_EINVAL, "n_poly must be at least 1, got %d", n_poly);
+    if (!a) return set_err(PSWE_EINVAL, "Chebyshev route needs n_poly + 1 coefficients");
+    TRY(c->a_dev.alloc((size_t)n_poly + 1));
+    CU(cudaMemcpy(c->a_dev.p, a, ((size_t)n_poly + 1) * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  c->kind = kind;
+  c->Lambda = Lambda;
+  c->n_poly = n_poly;
+  return PSWE_OK;
+}
+
+int pswe_compact_shape(const pswe_ctx* c, int* Ky, int* Kx) {
+  if (!c || !Ky || !Kx) return set_err(PSWE_EINVAL, "null argument");
+  *Ky = c->Ky;
+  *Kx = c->Kx;
+  return PSWE_OK;
+}
+
+int pswe_pack(pswe_ctx* c, const double* u, const double* v, const double* e, double* Uc, void* stream) {
+  if (!c || !u || !v || !e || !Uc) return set_err(PSWE_EINVAL, "null argument");
+  CU(cudaSetDevice(c->device));
+  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, (cudaStream_t)stream>>>(
+      c->grid(), (const double2*)u, (const double2*)v, (const double2*)e, (double2*)Uc);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+int pswe_unpack(pswe_ctx* c, const double* Uc, double* u, double* v, double* e, void* stream) {
+  if (!c || !u || !v || !e || !Uc) return set_err(PSWE_EINVAL, "null argument");
+  CU(cudaSetDevice(c->device));
+  unpack_kernel<<<elem_grid(c->full_elems()), 256, 0, (cudaStream_t)stream>>>(
+      c->grid(), (const double2*)Uc, (double2*)u, (double2*)v, (double2*)e);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+int pswe_averaged_tendency_compact(pswe_ctx* c, const double* Uc, double* Ac, void* stream) {
+  if (!c || !Uc || !Ac) return set_err(PSWE_EINVAL, "null argument");
+  if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
+  TRY(check_nodes(c));
+  CU(cudaSetDevice(c->device));
+  return rhs_compact(c, c->s_dev.p, c->w_dev.p, (int)c->s_live.size(), (const double2*)Uc, (double2*)Ac,
+                     (cudaStream_t)stream);
+}
+
+int pswe_averaged_tendency(pswe_ctx* c, const double* u, const double* v, const double* e, double* du,
+                           double* dv, double* de, void* stream) {
+  if (!c || !u || !v || !e || !du || !dv || !de) return set_err(PSWE_EINVAL, "null argument");
+  if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
+  TRY(check_nodes(c));
+  CU(cudaSetDevice(c->device));
+  TRY(ensure_compact(c));
+  TRY(pswe_pack(c, u, v, e, (double*)c->Uc.p, stream));
+  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, (int)c->s_live.size(), c->Uc.p, c->Ac.p, (cudaStream_t)stream));
+  return pswe_unpack(c, (const double*)c->Ac.p, du, dv, de, stream);
+}
+
+int pswe_apply_nonlinear(pswe_ctx* c, const double* u, const double* v, const double* e, double* du, double* dv,
+                         double* de, void* stream) {
+  if (!c || !u || !v || !e || !du || !dv || !de) return set_err(PSWE_EINVAL, "null argument");
+  CU(cudaSetDevice(c->device));
+  TRY(ensure_compact(c));
+  TRY(pswe_pack(c, u, v, e, (double*)c->Uc.p, stream));
+  TRY(rhs_compact(c, c->zero_s.p, c->one_w.p, 1, c->Uc.p, c->Ac.p, (cudaStream_t)stream));
+  return pswe_unpack(c, (const double*)c->Ac.p, du, dv, de, stream);
+}
+
+int pswe_apply_linear(pswe_ctx* c, const double* u, const double* v, const double* e, double* lu, double* lv,
+                      double* le, void* stream) {
+  if (!c || !u || !v || !e || !lu || !lv || !le) return set_err(PSWE_EINVAL, "null argument");
+  CU(cudaSetDevice(c->device));
+  linear_full_kernel<<<elem_grid(c->full_elems()), 256, 0, (cudaStream_t)stream>>>(c->grid(), f3(u, v, e),
+                                                                                  f3w(lu, lv, le));
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+int pswe_propagate(pswe_ctx* c, double t, const double* u, const double* v, const double* e, double* ou, double* ov,
+                   double* oe, void* stream) {
+  if (!c || !u || !v || !e || !ou || !ov || !oe) return set_err(PSWE_EINVAL, "null argument");
+  std::string msg;
+  if (check_cheb(c, t, &msg) != PSWE_OK) return set_err(PSWE_EINVAL, "%s", msg.c_str());
+  CU(cudaSetDevice(c->device));
+  propagate_full_kernel<<<elem_grid(c->full_elems()), 256, 0, (cudaStream_t)stream>>>(c->grid(), c->prop(), t,
+                                                                                     f3(u, v, e), f3w(ou, ov, oe));
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+int pswe_ssprk3_step(pswe_ctx* c, double dt, const double* u, const double* v, const double* e, double* ou,
+                     double* ov, double* oe, int* bad_stage, int* bad_field, void* stream) {
+  if (!c || !u || !v || !e || !ou || !ov || !oe) return set_err(PSWE_EINVAL, "null argument");
+  if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
+  if (!(dt > 0)) return set_err(PSWE_EINVAL, "dt must be positive, got %g", dt);
+  std::string msg;
+  if (check_cheb(c, dt, &msg) != PSWE_OK) return set_err(PSWE_EINVAL, "%s", msg.c_str());
+  TRY(check_nodes(c));
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
+  TRY(step_impl(c, dt, f3(u, v, e), f3w(ou, ov, oe), st));
+  CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  int stage = 0, field = -1;
+  if (decode_flags(*c->flags_host, &stage, &field)) {
+    if (bad_stage) *bad_stage = stage;
+    if (bad_field) *bad_field = field;
+    return set_err(PSWE_ENONFINITE, "non-finite values in field %s after stage %d", field_name(field), stage);
+  }
+  if (bad_stage) *bad_stage = 0;
+  if (bad_field) *bad_field = -1;
+  return PSWE_OK;
+}
+
+int pswe_run(pswe_ctx* c, double dt, int nsteps, double* u, double* v, double* e, int* bad_step, int* bad_stage,
+             int* bad_field, void* stream) {
+  if (!c || !u || !v || !e) return set_err(PSWE_EINVAL, "null argument");
+  if (nsteps < 0) return set_err(PSWE_EINVAL, "nsteps must be nonnegative, got %d", nsteps);
+  if (bad_step) *bad_step = 0;
+  if (nsteps == 0) return PSWE_OK;
+  if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
+  if (!(dt > 0)) return set_err(PSWE_EINVAL, "dt must be positive, got %g", dt);
+  std::string msg;
+  if (check_cheb(c, dt, &msg) != PSWE_OK) return set_err(PSWE_EINVAL, "%s", msg.c_str());
+  TRY(check_nodes(c));
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t n = c->full_elems();
+  TRY(c->full_tmp.alloc(n * 15));
+  double2* A = c->full_tmp.p + 9 * n;
+  double2* B = c->full_tmp.p + 12 * n;
+  CU(cudaMemcpyAsync(A, u, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(A + n, v, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(A + 2 * n, e, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  int rc = PSWE_OK;
+  for (int i = 1; i <= nsteps; ++i) {
+    CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
+    TRY(step_impl(c, dt, Full3{A, A + n, A + 2 * n}, Full3w{B, B + n, B + 2 * n}, st));
+    CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    int stage = 0, field = -1;
+    if (decode_flags(*c->flags_host, &stage, &field)) {
+      if (bad_step) *bad_step = i;
+      if (bad_stage) *bad_stage = stage;
+      if (bad_field) *bad_field = field;
+      rc = set_err(PSWE_ENONFINITE, "non-finite values in field %s after stage %d", field_name(field), stage);
+      break;
+    }
+    std::swap(A, B);
+  }
+  CU(cudaMemcpyAsync(u, A, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(v, A + n, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(e, A + 2 * n, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  return rc;
+}
+
+double pswe_max_frequency(const pswe_ctx* c) { return c ? c->lam_max : 0.0; }
+
+int64_t pswe_launch_count(const pswe_ctx* c) { return c ? c->launches : 0; }
+
+int pswe_profile_enable(pswe_ctx* c, int enable) {
+  if (!c) return set_err(PSWE_EINVAL, "null context");
+  c->prof = enable != 0;
+  return PSWE_OK;
+}
+
+int pswe_profile_read(pswe_ctx* c, double* ms, int64_t* launches, int n) {
+  if (!c) return set_err(PSWE_EINVAL, "null context");
+  CU(cudaSetDevice(c->device));
+  std::vector<double> acc(PSWE_NUM_KERNEL_CLASSES, 0.0);
+  std::vector<int64_t> cnt(PSWE_NUM_KERNEL_CLASSES, 0);
+  for (const auto& r : c->recs) {
+    CU(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, r.a, r.b));
+    acc[r.cls] += t;
+    cnt[r.cls] += 1;
+  }
+  c->recs.clear();
+  c->ev_used = 0;
+  for (int i = 0; i < n && i < PSWE_NUM_KERNEL_CLASSES; ++i) {
+    if (ms) ms[i] = acc[i];
+    if (launches) launches[i] = cnt[i];
+  }
+  return PSWE_OK;
+}
+
+int pswe_set_chunk_bytes(pswe_ctx* c, size_t bytes) {
+  if (!c) return set_err(PSWE_EINVAL, "null context");
+  c->chunk_bytes = std::max<size_t>(bytes, 1);
+  return PSWE_OK;
+}
+
+}  // extern "C"

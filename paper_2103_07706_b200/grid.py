@@ -1,0 +1,102 @@
+"""Spectral grid description (host side) mirroring ``phaseswe.grid``.
+
+Grid geometry and wavenumbers follow make_grid (grid.py:81-107).  The
+transform helpers here (``to_spectral``, ``to_physical``, ``dealias``) are
+host-side numpy utilities for building inputs and reading outputs, exactly as
+the reference offers them; none of them is on the B200 hot path, which runs
+its own fused FFT kernels behind the C ABI.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["SpectralGrid", "make_grid", "to_spectral", "to_physical", "dealias"]
+
+
+def _signed_index(n: int) -> np.ndarray:
+    # 0, 1, ..., n/2-1, -n/2, ..., -1  (numpy fftfreq order)
+    return np.fft.fftfreq(n, d=1.0 / n).astype(int)
+
+
+@dataclass(frozen=True)
+class SpectralGrid:
+    """Doubly periodic (nx, ny) grid on [0, Lx) x [0, Ly) (grid.py:34-73)."""
+
+    nx: int
+    ny: int
+    Lx: float
+    Ly: float
+    kx: np.ndarray = field(repr=False)
+    ky: np.ndarray = field(repr=False)
+    dealias_mask: np.ndarray = field(repr=False)
+
+    @property
+    def dx(self) -> float:
+        return self.Lx / self.nx
+
+    @property
+    def dy(self) -> float:
+        return self.Ly / self.ny
+
+    @property
+    def cell_area(self) -> float:
+        return self.dx * self.dy
+
+    @property
+    def x(self) -> np.ndarray:
+        return np.arange(self.nx) * self.dx
+
+    @property
+    def y(self) -> np.ndarray:
+        return np.arange(self.ny) * self.dy
+
+    def wavenumber_mesh(self):
+        return self.kx[:, None], self.ky[None, :]
+
+
+def make_grid(nx: int, ny: int, Lx: float, Ly: float) -> SpectralGrid:
+    """Validated grid; even n >= 8, positive lengths (grid.py:81-107)."""
+    for label, n in (("nx", nx), ("ny", ny)):
+        if n < 8 or n % 2 != 0:
+            raise ValueError(f"{label} must be even and >= 8, got {n}")
+    for label, length in (("Lx", Lx), ("Ly", Ly)):
+        if not length > 0:
+            raise ValueError(f"{label} must be positive, got {length}")
+    ix, iy = _signed_index(nx), _signed_index(ny)
+    kx = 2.0 * np.pi * ix / Lx
+    ky = 2.0 * np.pi * iy / Ly
+    band = (3 * np.abs(ix)[:, None] <= nx) & (3 * np.abs(iy)[None, :] <= ny)
+    for a in (kx, ky, band):
+        a.setflags(write=False)
+    return SpectralGrid(nx=nx, ny=ny, Lx=float(Lx), Ly=float(Ly), kx=kx, ky=ky, dealias_mask=band)
+
+
+def _shape_check(grid, a, what):
+    if a.shape != (grid.nx, grid.ny):
+        raise ValueError(f"{what} has shape {a.shape}, expected {(grid.nx, grid.ny)}")
+
+
+def to_spectral(grid: SpectralGrid, phys) -> np.ndarray:
+    """Host fft2 of a real field (grid.py:116-122); input construction only."""
+    phys = np.asarray(phys)
+    _shape_check(grid, phys, "physical field")
+    if np.iscomplexobj(phys):
+        raise ValueError("to_spectral expects a real-valued field")
+    return np.fft.fft2(phys.astype(np.float64, copy=False))
+
+
+def to_physical(grid: SpectralGrid, coeffs, scale=None) -> np.ndarray:
+    """Host real(ifft2) of Hermitian coefficients (grid.py:140-180 without the gate)."""
+    c = np.asarray(coeffs, dtype=np.complex128)
+    _shape_check(grid, c, "spectral field")
+    return np.fft.ifft2(c).real
+
+
+def dealias(grid: SpectralGrid, coeffs) -> np.ndarray:
+    """Zero the modes outside the 2/3 band (grid.py:183-187)."""
+    c = np.asarray(coeffs)
+    _shape_check(grid, c, "spectral field")
+    return np.where(grid.dealias_mask, c, 0.0)

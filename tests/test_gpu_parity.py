@@ -1,0 +1,236 @@
+"""GPU parity: the CUDA path against the reference's golden vectors and the oracle.
+
+Tolerances (north_star): relative L2 <= 1e-10 per averaged-RHS evaluation,
+<= 1e-8 after the named number of steps; unit operators are held to the
+reference's own test tolerances (1e-12 .. 1e-15).  Every call goes through
+the C ABI (libpswe_b200.so) via the drop-in Python API.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2103_07706_b200 as pk
+from conftest import load_golden, rel_l2
+from oracle import layout
+from oracle import pswe_oracle as O
+from paper_2103_07706_b200 import _native, cases
+
+pytestmark = pytest.mark.gpu
+
+F0, G0, H0 = 1.0e-4, 9.8, 5960.0
+RHS_TOL = 1e-10
+STEP_TOL = 1e-8
+
+
+def state_from(U, grid, t=0.0):
+    return pk.State(grid=grid, u=U[0], v=U[1], eta=U[2], t=t)
+
+
+def arr(st):
+    return np.stack([st.u, st.v, st.eta])
+
+
+def flat(grid):
+    return pk.PhysicsParams(f=F0, g=G0, H=H0, b=np.zeros((grid.nx, grid.ny), complex))
+
+
+def golden_problem(z):
+    nx, ny = int(z["nx"]), int(z["ny"])
+    grid = pk.make_grid(nx, ny, float(z["Lx"]), float(z["Ly"]))
+    b = layout.unpack(np.stack([z["b"]] * 3), nx, ny)[0]
+    params = pk.PhysicsParams(f=float(z["f"]), g=float(z["g"]), H=float(z["H"]), b=b)
+    state = state_from(layout.unpack(z["U"], nx, ny), grid)
+    quad = pk.kernel_weights(float(z["T_half"]), int(z["M"]))
+    return grid, params, state, quad
+
+
+# ---------------------------------------------------------------- unit operators
+def test_exact_exp_and_linear_match_reference_8x8(unit_golden):
+    g8 = pk.make_grid(8, 8, 1.0e6, 1.0e6)
+    st = state_from(unit_golden["exp8_U"], g8)
+    p = flat(g8)
+    for t, key in ((500.0, "exp8_p500"), (-250.0, "exp8_m250")):
+        out = pk.exact_exp(t, st, p)
+        want = unit_golden[key]
+        assert np.max(np.abs(arr(out) - want)) <= 1e-12 * np.max(np.abs(want))
+        assert out.t == t
+    lin = pk.apply_linear(st, p)
+    assert np.max(np.abs(arr(lin) - unit_golden["lin8"])) <= 1e-13 * np.max(np.abs(unit_golden["lin8"]))
+
+
+def test_nonlinear_matches_reference_8x8_with_topography(unit_golden):
+    g8 = pk.make_grid(8, 8, 1.0e6, 1.0e6)
+    p = pk.PhysicsParams(f=F0, g=G0, H=H0, b=unit_golden["nl8_b"])
+    out = pk.apply_nonlinear(state_from(unit_golden["nl8_U"], g8), p)
+    want = unit_golden["nl8_N"]
+    for f in range(3):
+        assert np.max(np.abs(arr(out)[f] - want[f])) <= 1e-12 * np.max(np.abs(want[f]))
+
+
+def test_averaged_tendency_32_exact_and_chebyshev(unit_golden):
+    g = pk.make_grid(32, 32, 4.0e7, 4.0e7)
+    st = state_from(layout.unpack(unit_golden["avg32_U"], 32, 32), g)
+    q = pk.kernel_weights(1800.0, 3)
+    got = pk.averaged_tendency(st, q, flat(g), pk.PropagatorSpec.exact())
+    assert rel_l2(layout.pack(arr(got)), unit_golden["avg32_exact"]) <= 1e-13
+    spec = pk.PropagatorSpec.chebyshev(float(unit_golden["avg32_cheb_Lambda"]))
+    assert spec.n_poly == int(unit_golden["avg32_cheb_npoly"])
+    got = pk.averaged_tendency(st, q, flat(g), spec)
+    assert rel_l2(layout.pack(arr(got)), unit_golden["avg32_cheb"]) <= 1e-13
+
+
+# ---------------------------------------------------------------- BASELINE configs
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_config_rhs_matches_reference(name):
+    z = load_golden(name)
+    grid, params, state, quad = golden_problem(z)
+    got = pk.averaged_tendency(state, quad, params, pk.PropagatorSpec.exact())
+    err = rel_l2(layout.pack(arr(got)), z["rhs"])
+    print(f"{name} RHS rel L2 {err:.3e}")
+    assert err <= RHS_TOL
+    assert got.t == state.t
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_config_steps_match_reference(name):
+    z = load_golden(name)
+    grid, params, state, quad = golden_problem(z)
+    cfg = pk.StepConfig(dt=float(z["dt"]), quadrature=quad, propagator_spec=pk.PropagatorSpec.exact())
+    one = pk.step_averaged_ssprk3(state, cfg, params)
+    err1 = rel_l2(layout.pack(arr(one)), z["step1"])
+    assert err1 <= STEP_TOL
+    assert one.t == float(z["dt"])
+    if "final" in z:
+        traj = pk.run(state, cfg, params, t_end=float(z["dt"]) * int(z["nsteps"]))
+        fin = traj.states[-1]
+        err = rel_l2(layout.pack(arr(fin)), z["final"])
+        print(f"{name}: step1 {err1:.3e}, after {int(z['nsteps'])} steps {err:.3e}")
+        assert err <= STEP_TOL
+        assert fin.t == float(z["t_final"])
+
+
+# ---------------------------------------------------------------- full sizes vs oracle
+def test_c5_512_rhs_matches_oracle():
+    c = cases.case_c5(7, 8)  # 512^2, 15 phases
+    got = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())
+    g = c.grid
+    S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, c.params.f, c.params.g, c.params.H)
+    q = c.quadrature
+    want = O.averaged_tendency(S, arr(c.state), q.s, q.w, workers=8)
+    err = O.rel_l2(arr(got), want)
+    print(f"C5 512^2 M=8 rel L2 vs oracle {err:.3e}")
+    assert err <= RHS_TOL
+
+
+def test_linearity_in_weights_at_512_m256():
+    """Full-size property: A(w_even + w_odd) = A(w_even) + A(w_odd) over all 511 phases."""
+    c = cases.case_c5(7, 256)
+    g, q = c.grid, c.quadrature
+    ctx = pk.dynamics.context(c.state, c.params)
+    ctx.set_propagator("exact")
+    U = pk.dynamics.upload(ctx, c.state)
+    Uc = ctx.pack(U)
+    w = np.array(q.w)
+    idx = np.arange(len(w))
+    parts = []
+    for sel in (idx % 2 == 0, idx % 2 == 1, np.ones_like(idx, bool)):
+        ctx.set_quadrature(q.s, np.where(sel, w, 0.0))
+        parts.append(ctx.averaged_tendency_compact(Uc).cpu().numpy())
+    assert rel_l2(parts[0] + parts[1], parts[2]) <= 1e-13
+    # run-to-run bitwise determinism of the full 511-phase evaluation
+    again = ctx.averaged_tendency_compact(Uc).cpu().numpy()
+    assert np.array_equal(again, parts[2])
+
+
+def test_chunking_does_not_change_results():
+    c = cases.case_c5(5, 32)  # 128^2, 63 phases
+    ctx = pk.dynamics.context(c.state, c.params)
+    ctx.set_propagator("exact")
+    ctx.set_quadrature(c.quadrature.s, c.quadrature.w)
+    Uc = ctx.pack(pk.dynamics.upload(ctx, c.state))
+    base = ctx.averaged_tendency_compact(Uc).cpu().numpy()
+    try:
+        ctx.set_chunk_bytes(1)  # one phase per chunk
+        one = ctx.averaged_tendency_compact(Uc).cpu().numpy()
+    finally:
+        ctx.set_chunk_bytes(40 << 20)
+    assert rel_l2(one, base) <= 1e-14
+
+
+def test_rectangular_grid_matches_oracle():
+    rng = np.random.default_rng(5)
+    g = pk.make_grid(64, 32, 4.0e7, 2.0e7)
+    S = O.Setup(64, 32, 4.0e7, 2.0e7, F0, G0, H0)
+    S.b = O.truncate(O.spectral(30.0 * rng.standard_normal((64, 32))), S.mask)
+    U = np.stack([O.truncate(O.spectral(sc * rng.standard_normal((64, 32))), S.mask) for sc in (1.0, 1.0, 50.0)])
+    p = pk.PhysicsParams(f=F0, g=G0, H=H0, b=S.b)
+    q = pk.kernel_weights(3600.0, 4)
+    got = pk.averaged_tendency(state_from(U, g), q, p, pk.PropagatorSpec.exact())
+    want = O.averaged_tendency(S, U, q.s, q.w)
+    assert O.rel_l2(arr(got), want) <= 1e-12
+
+
+# ---------------------------------------------------------------- edge cases
+def test_zero_window_equals_plain_nonlinearity_bitwise():
+    c = cases.case_c1()
+    got = pk.averaged_tendency(c.state, pk.kernel_weights(0.0, 0), c.params, pk.PropagatorSpec.exact())
+    want = pk.apply_nonlinear(c.state, c.params)
+    assert np.array_equal(arr(got), arr(want))
+
+
+def test_uniform_kernel_includes_endpoints():
+    c = cases.case_c1()
+    q = pk.kernel_weights(1800.0, 3, pk.UNIFORM_KERNEL)
+    got = pk.averaged_tendency(c.state, q, c.params, pk.PropagatorSpec.exact())
+    g = c.grid
+    S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, c.params.f, c.params.g, c.params.H)
+    assert O.rel_l2(arr(got), O.averaged_tendency(S, arr(c.state), q.s, q.w)) <= 1e-12
+
+
+def test_mean_eta_tendency_is_exactly_zero():
+    z = load_golden("C3")
+    grid, params, state, quad = golden_problem(z)
+    assert pk.apply_nonlinear(state, params).eta[0, 0] == 0.0
+    assert pk.averaged_tendency(state, quad, params, pk.PropagatorSpec.exact()).eta[0, 0] == 0.0
+
+
+def test_output_is_band_limited_and_hermitian():
+    c = cases.case_c1()
+    got = arr(pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact()))
+    mask = c.grid.dealias_mask
+    assert np.all(got[:, ~mask] == 0.0)
+    refl = np.roll(np.flip(got, axis=(1, 2)), shift=(1, 1), axis=(1, 2))
+    assert np.max(np.abs(got - np.conj(refl))) <= 1e-13 * np.max(np.abs(got))
+
+
+def test_unsupported_grid_is_refused():
+    g = pk.make_grid(48, 48, 4.0e7, 4.0e7)
+    st = pk.State(grid=g, u=np.zeros((48, 48)), v=np.zeros((48, 48)), eta=np.zeros((48, 48)))
+    with pytest.raises(ValueError, match="not supported by the B200 path"):
+        pk.apply_nonlinear(st, flat(g))
+
+
+def test_chebyshev_window_violation_names_the_node():
+    c = cases.case_c1()
+    spec = pk.PropagatorSpec.chebyshev(pk.max_frequency(c.grid, c.params) * 100.0)
+    with pytest.raises(RuntimeError, match=r"averaging node k = -7 .*exceeds Lambda"):
+        pk.averaged_tendency(c.state, c.quadrature, c.params, spec)
+
+
+def test_nonfinite_state_aborts_with_stage_and_field():
+    c = cases.case_c1()
+    u = c.state.u.copy()
+    u[40 % 32, 3] = np.inf
+    bad = pk.State(grid=c.grid, u=u, v=c.state.v, eta=c.state.eta)
+    cfg = pk.make_step_config(c.grid, c.params, dt=600.0)
+    with pytest.raises(RuntimeError, match="non-finite values in field u after stage 1"):
+        pk.step_averaged_ssprk3(bad, cfg, c.params)
+
+
+def test_native_code_is_what_ran():
+    c = cases.case_c1()
+    ctx = pk.dynamics.context(c.state, c.params)
+    before = ctx.launch_count
+    pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())
+    assert ctx.launch_count > before
+    assert _native._lib is not None
