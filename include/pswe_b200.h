@@ -23,7 +23,7 @@
  *  - Return value: 0 on success, nonzero on error; pswe_last_error() gives a
  *    thread-local message.  Errors from argument validation use the
  *    reference's wording where the reference raises.
- *  - Grid sizes: nx, ny powers of two in [8, 1024] (the reference allows
+ *  - Grid sizes: nx, ny powers of two in [8, 512] (the reference allows
  *    any even n >= 8, grid.py:91-93; other sizes return PSWE_EUNSUPPORTED).
  *  - Threading: a context may be used by one host thread at a time.
  */

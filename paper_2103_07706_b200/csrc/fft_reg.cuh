@@ -94,6 +94,25 @@ __device__ __forceinline__ void group_sync(int group_in_cta) {
 // Butterfly j in [0, N/R): inputs x[j + r*N/R], twiddle W_N^{r*(j%NS)*N/(NS*R)},
 // outputs x'[(j/NS)*NS*R + j%NS + r*NS].  Thread t does butterflies
 // j = t + q*N/8, q < 8/R, with registers v[q*R + r].
+// Twiddles W^{r e}, r = 1..R-1, from one table entry W^e by a depth-3 power
+// tree (w2 = w1^2, w4 = w2^2, ...): one shared-memory load per butterfly
+// instead of R-1 dependent global loads.
+template <int R, bool INV>
+__device__ __forceinline__ void twiddle_powers(double2 w1, double2* w) {
+  if (INV) w1.y = -w1.y;
+  w[1] = w1;
+  if constexpr (R >= 4) {
+    w[2] = cmul(w1, w1);
+    w[3] = cmul(w[2], w1);
+  }
+  if constexpr (R == 8) {
+    w[4] = cmul(w[2], w[2]);
+    w[5] = cmul(w[4], w1);
+    w[6] = cmul(w[3], w[3]);
+    w[7] = cmul(w[4], w[3]);
+  }
+}
+
 template <int N, int R, int NS, bool INV>
 __device__ __forceinline__ void stage_compute(double2* v, int t, const double2* __restrict__ tw) {
   constexpr int B = 8 / R;
@@ -102,12 +121,10 @@ __device__ __forceinline__ void stage_compute(double2* v, int t, const double2* 
     if constexpr (NS > 1) {
       const int j = t + q * (N / 8);
       const int k = j % NS;
+      double2 w[8];
+      twiddle_powers<R, INV>(tw[k * (N / (NS * R))], w);
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        double2 w = __ldg(tw + r * k * (N / (NS * R)));
-        if (INV) w.y = -w.y;
-        v[q * R + r] = cmul(v[q * R + r], w);
-      }
+      for (int r = 1; r < R; ++r) v[q * R + r] = cmul(v[q * R + r], w[r]);
     }
     dftR<R, INV>(v + q * R);
   }
@@ -194,14 +211,21 @@ struct Stages {
 };
 
 // Full transform: v[m] = x[t + m*N/8] in, X[t + m*N/8] out.  sm: group's padded
-// exchange buffer (FFTSize<N>::PAD double2).  Contains group barriers: every
-// thread of the group must call it.
+// exchange buffer (FFTSize<N>::PAD double2); tw: the N-entry forward twiddle
+// table W_N^k, normally staged in shared memory (load_twiddles).  Contains
+// group barriers: every thread of the group must call it.
 template <int N, bool INV>
 __device__ __forceinline__ void fft_reg(double2* v, int t, double2* sm, int gid,
                                         const double2* __restrict__ tw) {
   constexpr int R0 = StageRadix<N, 1>::R;
   to_stage_layout<R0>(v);
   Stages<N, 1, INV>::run(v, t, sm, gid, tw);
+}
+
+// copy the N-entry twiddle table to shared memory (whole CTA; caller syncs)
+template <int N>
+__device__ __forceinline__ void load_twiddles(double2* dst, const double2* __restrict__ src) {
+  for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = src[i];
 }
 
 }  // namespace pswe

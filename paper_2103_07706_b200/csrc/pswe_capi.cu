@@ -44,7 +44,7 @@ int set_err(int code, const char* fmt, ...) {
     if (rc_ != PSWE_OK) return rc_; \
   } while (0)
 
-bool pow2_ok(int n) { return n >= 8 && n <= 1024 && (n & (n - 1)) == 0; }
+bool pow2_ok(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
 
 template <typename T>
 struct DevBuf {
@@ -152,18 +152,15 @@ struct ProfScope {
 };
 
 // ---------------------------------------------------------------- dispatch
-template <int N>
-constexpr int groups_per_cta() {
-  return (1024 / N) > 0 ? (1024 / N) : 1;
-}
-
 template <int NX>
 int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, cudaStream_t st) {
-  constexpr int GPC = groups_per_cta<NX>();
-  const int tasks = np * c->Ky;
-  const int blocks = (tasks + GPC - 1) / GPC;
+  using W = PassAW<NX>;
+  const size_t smem = W::bytes(c->Kx);
+  auto kern = passA_kernel<NX>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int blocks = (np * c->Ky + W::GPW - 1) / W::GPW;
   ProfScope ps(c, 0, st);
-  passA_kernel<NX, GPC><<<blocks, GPC * NX / 8, 0, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->inter.p);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->inter.p);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -171,29 +168,27 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
 
 template <int NY>
 int launchB(pswe_ctx* c, int np, cudaStream_t st) {
-  constexpr int G = groups_per_cta<NY>();
-  const size_t smem = ((size_t)5 * c->Ky * G + (size_t)G * FFTSize<NY>::PAD) * sizeof(double2);
-  auto kern = passB_kernel<NY, G>;
+  using W = PassBW<NY>;
+  const size_t smem = W::bytes();
+  auto kern = passB_kernel<NY>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int tasks = np * c->nx;
-  const int blocks = (tasks + G - 1) / G;
+  const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, G * NY / 8, smem, st>>>(c->grid(), np, c->inter.p);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, c->inter.p);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
 
 template <int NX>
-int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, cudaStream_t st) {
-  constexpr int GPC = groups_per_cta<NX>();
-  const size_t smem = (size_t)GPC * (FFTSize<NX>::PAD + 7 * c->Kx) * sizeof(double2);
-  auto kern = passC_kernel<NX, GPC>;
+int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int first, cudaStream_t st) {
+  using W = PassCW<NX>;
+  const size_t smem = W::bytes(c->Kx);
+  auto kern = passC_kernel<NX>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int tasks = c->Ky * Gc;
-  const int blocks = (tasks + GPC - 1) / GPC;
+  const int blocks = (np * c->Ky + W::GPW - 1) / W::GPW;
   ProfScope ps(c, 2, st);
-  kern<<<blocks, GPC * NX / 8, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, c->inter.p, c->slots.p, first);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, c->inter.p, c->slots.p, first);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -208,7 +203,6 @@ int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc
     case 128: return launchA<128>(c, ph, p0, np, Uc, st);
     case 256: return launchA<256>(c, ph, p0, np, Uc, st);
     case 512: return launchA<512>(c, ph, p0, np, Uc, st);
-    case 1024: return launchA<1024>(c, ph, p0, np, Uc, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
@@ -221,20 +215,18 @@ int dispatchB(pswe_ctx* c, int np, cudaStream_t st) {
     case 128: return launchB<128>(c, np, st);
     case 256: return launchB<256>(c, np, st);
     case 512: return launchB<512>(c, np, st);
-    case 1024: return launchB<1024>(c, np, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported ny = %d", c->ny);
 }
-int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, cudaStream_t st) {
+int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int first, cudaStream_t st) {
   switch (c->nx) {
-    case 8: return launchC<8>(c, ph, p0, np, Gc, first, st);
-    case 16: return launchC<16>(c, ph, p0, np, Gc, first, st);
-    case 32: return launchC<32>(c, ph, p0, np, Gc, first, st);
-    case 64: return launchC<64>(c, ph, p0, np, Gc, first, st);
-    case 128: return launchC<128>(c, ph, p0, np, Gc, first, st);
-    case 256: return launchC<256>(c, ph, p0, np, Gc, first, st);
-    case 512: return launchC<512>(c, ph, p0, np, Gc, first, st);
-    case 1024: return launchC<1024>(c, ph, p0, np, Gc, first, st);
+    case 8: return launchC<8>(c, ph, p0, np, first, st);
+    case 16: return launchC<16>(c, ph, p0, np, first, st);
+    case 32: return launchC<32>(c, ph, p0, np, first, st);
+    case 64: return launchC<64>(c, ph, p0, np, first, st);
+    case 128: return launchC<128>(c, ph, p0, np, first, st);
+    case 256: return launchC<256>(c, ph, p0, np, first, st);
+    case 512: return launchC<512>(c, ph, p0, np, first, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
@@ -246,9 +238,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   const size_t per_phase = (size_t)5 * c->Ky * c->nx;  // double2 elements
   int CP = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
   CP = std::min(CP, P);
-  const int target_groups = 2 * 148;
-  int Gc = std::max(1, (target_groups + c->Ky - 1) / c->Ky);
-  Gc = std::min(Gc, CP);
+  const int Gc = CP;  // one accumulation slot per phase position in a chunk
   TRY(c->inter.alloc(per_phase * CP));
   TRY(c->slots.alloc((size_t)Gc * c->compact_elems()));
   PhaseDev ph{s, w, P};
@@ -256,7 +246,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     const int np = std::min(CP, P - p0);
     TRY(dispatchA(c, ph, p0, np, Uc, st));
     TRY(dispatchB(c, np, st));
-    TRY(dispatchC(c, ph, p0, np, Gc, p0 == 0 ? 1 : 0, st));
+    TRY(dispatchC(c, ph, p0, np, p0 == 0 ? 1 : 0, st));
   }
   const size_t n = c->compact_elems();
   ProfScope ps(c, 3, st);
@@ -371,7 +361,7 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
   if (!(H > 0)) return set_err(PSWE_EINVAL, "H must be positive, got %g", H);
   if (!pow2_ok(nx) || !pow2_ok(ny))
     return set_err(PSWE_EUNSUPPORTED,
-                   "grid %dx%d not supported by the B200 path (nx, ny must be powers of two in [8, 1024])", nx, ny);
+                   "grid %dx%d not supported by the B200 path (nx, ny must be powers of two in [8, 512])", nx, ny);
   CU(cudaSetDevice(device));
   pswe_ctx* c = new pswe_ctx();
   c->device = device;

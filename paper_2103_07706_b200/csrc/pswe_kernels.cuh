@@ -8,8 +8,9 @@
 //             r = compact kx index 0..Kx-1 (wx = r for r <= KXM, r - Kx after).
 //             Only the 2/3 band |wx| <= nx/3, |wy| <= ny/3 (grid.py:102-103)
 //             is stored; the ky < 0 half is the conjugate mirror.
-//   I (chunk intermediates): I[p][f][j][x], p = phase in chunk, f in 0..4,
-//             j = 0..KYM, x = 0..nx-1 (physical x, spectral y).
+//   I (chunk intermediates): I[p][x][f][j], p = phase in chunk, x = 0..nx-1
+//             (physical x), f in 0..4, j = 0..KYM (spectral y): one physical
+//             row's five half-spectra are contiguous for pass B.
 //
 // Averaged RHS (averaging.py:116-156) for a chunk of phases:
 //   pass A  (per phase, ky column)  e^{sL} per mode + 5 inverse x-FFTs
@@ -19,7 +20,7 @@
 //                                   truncation, e^{-sL}, weighted ordered sum
 // followed by an ordered reduction over the phase-group slots.
 #pragma once
-#include "fft_reg.cuh"
+#include "wfft.cuh"
 
 namespace pswe {
 
@@ -49,66 +50,80 @@ __device__ __forceinline__ int band_r(int k, int n, int kxm, int Kx) {
   return -1;
 }
 
+// I[p][x][f][j]
+__device__ __forceinline__ size_t iidx(const GridDev& G, int pl, int x, int f, int j) {
+  return (((size_t)pl * G.nx + x) * 5 + f) * G.Ky + j;
+}
+
 __device__ __forceinline__ size_t cidx(const GridDev& G, int f, int j, int r) {
   return ((size_t)f * G.Ky + j) * G.Kx + r;
 }
 
 // ============================================================================
-// pass A: e^{s L} + inverse x-FFT of u, v, eta-b, ikx u, ikx v for one column
+// pass A: e^{s L} + inverse x-FFT of u, v, eta-b, ikx u, ikx v.
+// One CTA = 5 warps; warp f owns output field f for the CTA's GPW tasks
+// (task = one (phase, ky column)); the e^{sL} per mode is computed once per
+// task by the whole CTA into a shared compact stash.
 // ============================================================================
-template <int NX, int GPC>
-__global__ void __launch_bounds__(GPC* NX / 8)
+template <int NX>
+struct PassAW {
+  static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
+  static constexpr int WARPS = 5;
+  static size_t bytes(int Kx) {
+    return (size_t)GPW * 3 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
+  }
+};
+
+template <int NX>
+__global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
     passA_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, const double2* __restrict__ Uc,
                  double2* __restrict__ I) {
-  constexpr int T = NX / 8;
-  constexpr int PAD = FFTSize<NX>::PAD;
-  __shared__ double2 sm[GPC][PAD];
-  const int gid = threadIdx.x / T, t = threadIdx.x % T;
-  const int task = blockIdx.x * GPC + gid;
-  const bool active = task < np * G.Ky;
-  const int pl = active ? task / G.Ky : 0;
-  const int j = active ? task % G.Ky : 0;
-  const double s = active ? ph.s[p0 + pl] : 0.0;
-  const double ky = G.kyc[j];
+  using W = PassAW<NX>;
+  constexpr int T = W::T, P = W::P, GPW = W::GPW;
+  extern __shared__ double2 dsm[];
+  const int Kx = G.Kx, Ky = G.Ky;
+  double2* stash = dsm;  // [GPW][3][Kx], already scaled by 1/(nx ny)
+  double* xbuf = reinterpret_cast<double*>(dsm + (size_t)GPW * 3 * Kx);
+  const int ntask = np * Ky;
 
-  double2 uu[8], vv[8], dd[8];
-  double kxv[8];
+  // e^{s L} once per (task, mode)
+  for (int idx = threadIdx.x; idx < GPW * Kx; idx += blockDim.x) {
+    const int tl = idx / Kx, r = idx % Kx;
+    const int task = blockIdx.x * GPW + tl;
+    C3 q = c3zero();
+    if (task < ntask) {
+      const int pl = task / Ky, j = task % Ky;
+      q = {Uc[cidx(G, 0, j, r)], Uc[cidx(G, 1, j, r)], Uc[cidx(G, 2, j, r)]};
+      q = expL(ph.s[p0 + pl], q, G.ph, G.kxc[r], G.kyc[j], pr);
+      q.e = csub(q.e, G.bc[(size_t)j * Kx + r]);
+    }
+    double2* st = stash + (size_t)tl * 3 * Kx;
+    st[r] = cscale(G.inv_n2, q.u);
+    st[Kx + r] = cscale(G.inv_n2, q.v);
+    st[2 * Kx + r] = cscale(G.inv_n2, q.e);
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;  // warp = field
+  const int tl = lane / T, t = lane % T;
+  const int task = blockIdx.x * GPW + tl;
+  const bool active = task < ntask;
+  const int pl = active ? task / Ky : 0, j = active ? task % Ky : 0;
+  const double2* st = stash + (size_t)tl * 3 * Kx + (f < 3 ? f : f - 3) * Kx;
+  double2 v[P];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const int r = band_r(t + m * T, NX, G.kxm, G.Kx);
-    uu[m] = vv[m] = dd[m] = czero();
-    kxv[m] = 0.0;
-    if (active && r >= 0) {
-      C3 q = {Uc[cidx(G, 0, j, r)], Uc[cidx(G, 1, j, r)], Uc[cidx(G, 2, j, r)]};
-      const double kx = G.kxc[r];
-      q = expL(s, q, G.ph, kx, ky, pr);
-      const double2 b = G.bc[(size_t)j * G.Kx + r];
-      uu[m] = cscale(G.inv_n2, q.u);
-      vv[m] = cscale(G.inv_n2, q.v);
-      dd[m] = cscale(G.inv_n2, csub(q.e, b));
-      kxv[m] = kx;
+  for (int n1 = 0; n1 < P; ++n1) {
+    const int r = band_r(t + T * n1, NX, G.kxm, Kx);
+    v[n1] = czero();
+    if (r >= 0) {
+      v[n1] = st[r];
+      if (f >= 3) v[n1] = cik(G.kxc[r], v[n1]);
     }
   }
-  double2* out = I + ((size_t)pl * 5 * G.Ky + j) * NX;
-  const size_t fstride = (size_t)G.Ky * NX;
-#pragma unroll 1
-  for (int f = 0; f < 5; ++f) {
-    double2 v[8];
+  wfft_t1<NX, true>(v, t, xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF, G.twx);
+  if (active) {
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      switch (f) {
-        case 0: v[m] = uu[m]; break;
-        case 1: v[m] = vv[m]; break;
-        case 2: v[m] = dd[m]; break;
-        case 3: v[m] = cik(kxv[m], uu[m]); break;
-        default: v[m] = cik(kxv[m], vv[m]); break;
-      }
-    }
-    fft_reg<NX, true>(v, t, sm[gid], gid, G.twx);
-    if (active) {
-#pragma unroll
-      for (int m = 0; m < 8; ++m) out[f * fstride + t + m * T] = v[m];
-    }
+    for (int i = 0; i < P; ++i) I[iidx(G, pl, t1_pos<NX>(t, i), f, j)] = v[i];
   }
 }
 
@@ -116,19 +131,35 @@ __global__ void __launch_bounds__(GPC* NX / 8)
 // pass B: per physical row x: y-C2R of the 7 fields (paired by physical
 // dimension: (u,v), (ux,uy), (vx,vy), (depth,0)), quadratic products, y-R2C
 // of (A,B) and (C,D), keep ky = 0..KYM.  In place on I (fields 0..3 out).
+// Pairing by dimension matters: a pair's round-off is relative to the larger
+// member, so (depth [m], ux [1/s]) would cost ~1e-10 relative in ux.
+// One transform group (T lanes, 16 points each) per row; the products are
+// formed on the y positions each lane owns between the type-1 (inverse) and
+// type-2 (forward) transforms.
 // ============================================================================
 template <int NY>
-__device__ __forceinline__ void load_pair(double2* v, int t, const double2* tile, int G, int g,
-                                          int Ky, int kym, int fa, int fb, int deriv_b,
-                                          const double* __restrict__ kyc) {
-  // Z[k] = A[k] + i B[k] (k <= KYM), conj(A[-k]) + i conj(B[-k]) (k >= NY-KYM)
-  // fa, fb: tile field indices (fb < 0: B = 0); deriv_b: B = i ky * tile[fb].
-  constexpr int T = NY / 8;
+struct PassBW {
+  static constexpr int T = WF<NY>::T, P = WF<NY>::P, GPW = WF<NY>::GPW;
+  static constexpr int WARPS = 4;
+  static constexpr int GPC = WARPS * GPW;  // rows per CTA
+  static size_t bytes() {
+    return (size_t)GPC * (WF<NY>::XBUF * sizeof(double) + (size_t)P * T * sizeof(double2));
+  }
+};
+
+// type-1 input of the packed pair A + iB at positions k = t + T n1
+template <int NY>
+__device__ __forceinline__ void load_row_pair(double2* v, int t, const double2* row, int Ky, int kym, int fa,
+                                              int fb, int deriv_b, const double* __restrict__ kyc,
+                                              bool active) {
+  constexpr int T = WF<NY>::T, P = WF<NY>::P;
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const int k = t + m * T;
+  for (int n1 = 0; n1 < P; ++n1) {
+    const int k = t + T * n1;
     int jj;
     bool cj;
+    v[n1] = czero();
+    if (!active) continue;
     if (k <= kym) {
       jj = k;
       cj = false;
@@ -136,182 +167,174 @@ __device__ __forceinline__ void load_pair(double2* v, int t, const double2* tile
       jj = NY - k;
       cj = true;
     } else {
-      v[m] = czero();
       continue;
     }
-    double2 A = tile[((size_t)fa * Ky + jj) * G + g];
+    const double2 A = row[fa * Ky + jj];
     double2 B = czero();
     if (fb >= 0) {
-      B = tile[((size_t)fb * Ky + jj) * G + g];
+      B = row[fb * Ky + jj];
       if (deriv_b) B = cik(__ldg(kyc + jj), B);
     }
     if (jj == 0) {
-      v[m] = cmk(A.x, B.x);  // Hermitian projection of the y-mean bin
+      v[n1] = cmk(A.x, B.x);  // Hermitian projection of the y-mean bin
     } else if (!cj) {
-      v[m] = cmk(A.x - B.y, A.y + B.x);
+      v[n1] = cmk(A.x - B.y, A.y + B.x);
     } else {
-      v[m] = cmk(A.x + B.y, B.x - A.y);
+      v[n1] = cmk(A.x + B.y, B.x - A.y);
     }
   }
 }
 
-template <int NY, int G>
-__global__ void __launch_bounds__(G* NY / 8)
+// after a type-2 forward transform (v[k2] = Z[t + T k2]): split the packed pair
+// into the two real spectra X = (Z + conj Z(-j))/2, Y = (Z - conj Z(-j))/(2i)
+// for j = 0..Ky-1 and store them.
+template <int NY>
+__device__ __forceinline__ void unpack_store(const double2* v, int t, double2* outX, double2* outY, int Ky,
+                                             bool active) {
+  constexpr int T = WF<NY>::T, P = WF<NY>::P;
+  constexpr int MU = (NY / 3 + 1 + T - 1) / T;
+#pragma unroll
+  for (int m = 0; m < MU; ++m) {
+    const int j = t + T * m;
+    double2 zm;
+    if constexpr (T == 1) {
+      zm = v[(P - m) & (P - 1)];
+    } else {
+      const double2 src = v[P - 1 - m];
+      double2 r;
+      r.x = __shfl_sync(0xffffffffu, src.x, (T - t) & (T - 1), T);
+      r.y = __shfl_sync(0xffffffffu, src.y, (T - t) & (T - 1), T);
+      zm = t == 0 ? v[(P - m) & (P - 1)] : r;
+    }
+    if (active && j < Ky) {
+      const double2 a = v[m];
+      outX[j] = cmk(0.5 * (a.x + zm.x), 0.5 * (a.y - zm.y));
+      outY[j] = cmk(0.5 * (a.y + zm.y), -0.5 * (a.x - zm.x));
+    }
+  }
+}
+
+template <int NY>
+__global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     passB_kernel(GridDev Gd, int np, double2* __restrict__ I) {
-  constexpr int T = NY / 8;
-  constexpr int PAD = FFTSize<NY>::PAD;
+  using W = PassBW<NY>;
+  constexpr int T = W::T, P = W::P;
   extern __shared__ double2 dsm[];
-  const int Ky = Gd.Ky, NX = Gd.nx;
-  double2* tile = dsm;                        // [5][Ky][G]
-  double2* xs = dsm + (size_t)5 * Ky * G;     // [G][PAD]
-  const int gid = threadIdx.x / T, t = threadIdx.x % T;
-  const int ntask = np * NX;
-  const size_t fstride = (size_t)Ky * NX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane % T;
+  const int group = warp * W::GPW + lane / T;
+  double2* uv = dsm + (size_t)group * P * T;  // [P][T] physical (u, v) at this lane's positions
+  double* xb = reinterpret_cast<double*>(dsm + (size_t)W::GPC * P * T) + (size_t)group * WF<NY>::XBUF;
+  const int Ky = Gd.Ky;
+  const int task = blockIdx.x * W::GPC + group;
+  const bool active = task < np * Gd.nx;
+  double2* row = I + (size_t)(active ? task : 0) * 5 * Ky;
 
-  // cooperative, x-contiguous load of the 5 input fields for G rows
-  for (int idx = threadIdx.x; idx < 5 * Ky * G; idx += blockDim.x) {
-    const int g = idx % G, fj = idx / G;
-    const int f = fj / Ky, jj = fj % Ky;
-    const int task = blockIdx.x * G + g;
-    double2 val = czero();
-    if (task < ntask) {
-      const int pl = task / NX, x = task % NX;
-      val = I[((size_t)pl * 5 + f) * fstride + (size_t)jj * NX + x];
-    }
-    tile[idx] = val;
-  }
-  __syncthreads();
-
-  double2* sm = xs + (size_t)gid * PAD;
-  double pu[8], pv[8], pa[8], pb[8];
-  double2 v[8];
+  double2 v[P];
+  double pa[P];
   // (u, v)
-  load_pair<NY>(v, t, tile, G, gid, Ky, Gd.kym, 0, 1, 0, Gd.kyc);
-  fft_reg<NY, true>(v, t, sm, gid, Gd.twy);
+  load_row_pair<NY>(v, t, row, Ky, Gd.kym, 0, 1, 0, Gd.kyc, active);
+  wfft_t1<NY, true>(v, t, xb, Gd.twy);
 #pragma unroll
-  for (int m = 0; m < 8; ++m) { pu[m] = v[m].x; pv[m] = v[m].y; }
+  for (int i = 0; i < P; ++i) uv[i * T + t] = v[i];
   // (ux, uy): A = -(u ux + v uy)
-  load_pair<NY>(v, t, tile, G, gid, Ky, Gd.kym, 3, 0, 1, Gd.kyc);
-  fft_reg<NY, true>(v, t, sm, gid, Gd.twy);
+  load_row_pair<NY>(v, t, row, Ky, Gd.kym, 3, 0, 1, Gd.kyc, active);
+  wfft_t1<NY, true>(v, t, xb, Gd.twy);
 #pragma unroll
-  for (int m = 0; m < 8; ++m) pa[m] = -(pu[m] * v[m].x + pv[m] * v[m].y);
+  for (int i = 0; i < P; ++i) {
+    const double2 q = uv[i * T + t];
+    pa[i] = -(q.x * v[i].x + q.y * v[i].y);
+  }
   // (vx, vy): B = -(u vx + v vy)
-  load_pair<NY>(v, t, tile, G, gid, Ky, Gd.kym, 4, 1, 1, Gd.kyc);
-  fft_reg<NY, true>(v, t, sm, gid, Gd.twy);
+  load_row_pair<NY>(v, t, row, Ky, Gd.kym, 4, 1, 1, Gd.kyc, active);
+  wfft_t1<NY, true>(v, t, xb, Gd.twy);
 #pragma unroll
-  for (int m = 0; m < 8; ++m) pb[m] = -(pu[m] * v[m].x + pv[m] * v[m].y);
+  for (int i = 0; i < P; ++i) {
+    const double2 q = uv[i * T + t];
+    v[i] = cmk(pa[i], -(q.x * v[i].x + q.y * v[i].y));
+  }
+  wfft_t2<NY, false>(v, t, xb, Gd.twy);
+  __syncwarp();  // every lane of the group has read fields 0..4 it needs from row
+  unpack_store<NY>(v, t, row, row + Ky, Ky, active);
   // (depth, 0): C = u depth, D = v depth
-  load_pair<NY>(v, t, tile, G, gid, Ky, Gd.kym, 2, -1, 0, Gd.kyc);
-  fft_reg<NY, true>(v, t, sm, gid, Gd.twy);
-  double2 z2[8];
+  load_row_pair<NY>(v, t, row, Ky, Gd.kym, 2, -1, 0, Gd.kyc, active);
+  wfft_t1<NY, true>(v, t, xb, Gd.twy);
 #pragma unroll
-  for (int m = 0; m < 8; ++m) z2[m] = cmk(pu[m] * v[m].x, pv[m] * v[m].x);
-  __syncthreads();  // every group is done reading the input tile
-  double2* otile = tile;  // [4][Ky][G]
-
-  // forward transforms of A + iB and C + iD, split into the two real spectra
-#pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 0) {
-#pragma unroll
-      for (int m = 0; m < 8; ++m) v[m] = cmk(pa[m], pb[m]);
-    } else {
-#pragma unroll
-      for (int m = 0; m < 8; ++m) v[m] = z2[m];
-    }
-    fft_reg<NY, false>(v, t, sm, gid, Gd.twy);
-    group_sync<NY>(gid);
-#pragma unroll
-    for (int m = 0; m < 8; ++m) sm[pidx(t + m * T)] = v[m];
-    group_sync<NY>(gid);
-    for (int jj = t; jj < Ky; jj += T) {
-      const double2 a = sm[pidx(jj)];
-      const double2 b = sm[pidx((NY - jj) & (NY - 1))];
-      // X = (a + conj b)/2, Y = (a - conj b)/(2i)
-      const double2 X = cmk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
-      const double2 Y = cmk(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
-      otile[((size_t)(2 * pass) * Ky + jj) * G + gid] = X;
-      otile[((size_t)(2 * pass + 1) * Ky + jj) * G + gid] = Y;
-    }
+  for (int i = 0; i < P; ++i) {
+    const double2 q = uv[i * T + t];
+    v[i] = cmk(q.x * v[i].x, q.y * v[i].x);
   }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < 4 * Ky * G; idx += blockDim.x) {
-    const int g = idx % G, fj = idx / G;
-    const int f = fj / Ky, jj = fj % Ky;
-    const int task = blockIdx.x * G + g;
-    if (task < ntask) {
-      const int pl = task / NX, x = task % NX;
-      I[((size_t)pl * 5 + f) * fstride + (size_t)jj * NX + x] = otile[idx];
-    }
-  }
+  wfft_t2<NY, false>(v, t, xb, Gd.twy);
+  __syncwarp();
+  unpack_store<NY>(v, t, row + 2 * Ky, row + 3 * Ky, Ky, active);
 }
 
 // ============================================================================
-// pass C: forward x-FFT of the 4 product spectra of one ky column, flux
-// divergence, 2/3 truncation, e^{-sL}, weighted sum over this group's phases
-// in ascending order onto the group's slot (averaging.py:148-155).
+// pass C: forward x-FFT of the 4 product spectra (warp f = field f) of the
+// CTA's GPW tasks (phase, ky column), then per mode: flux divergence, 2/3
+// truncation, e^{-sL}, weight, and accumulation onto the phase's slot
+// (slot g = phase position in the chunk; chunks are summed in order and the
+// slots reduced in order afterwards -- deterministic, no atomics).
 // ============================================================================
-template <int NX, int GPC>
-__global__ void __launch_bounds__(GPC* NX / 8)
-    passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I,
+template <int NX>
+struct PassCW {
+  static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
+  static constexpr int WARPS = 4;
+  static size_t bytes(int Kx) {
+    return (size_t)GPW * 4 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
+  }
+};
+
+template <int NX>
+__global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
+    passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, const double2* __restrict__ I,
                  double2* __restrict__ slots, int first_chunk) {
-  constexpr int T = NX / 8;
-  constexpr int PAD = FFTSize<NX>::PAD;
+  using W = PassCW<NX>;
+  constexpr int T = W::T, P = W::P, GPW = W::GPW;
   extern __shared__ double2 dsm[];
   const int Kx = G.Kx, Ky = G.Ky;
-  const int gid = threadIdx.x / T, t = threadIdx.x % T;
-  const int per_group = PAD + 7 * Kx;
-  double2* sm = dsm + (size_t)gid * per_group;  // exchange
-  double2* F = sm + PAD;                          // [4][Kx]
-  double2* acc = F + 4 * Kx;                      // [3][Kx]
-  const int task = blockIdx.x * GPC + gid;
-  const bool active = task < Ky * Gc;
-  const int j = active ? task % Ky : 0;
-  const int g = active ? task / Ky : 0;
-  const int lo = (int)(((long long)g * np) / Gc), hi = (int)(((long long)(g + 1) * np) / Gc);
-  const double ky = G.kyc[j];
+  double2* F = dsm;  // [GPW][4][Kx]
+  double* xbuf = reinterpret_cast<double*>(dsm + (size_t)GPW * 4 * Kx);
+  const int ntask = np * Ky;
+  {
+    const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;
+    const int tl = lane / T, t = lane % T;
+    const int task = blockIdx.x * GPW + tl;
+    const bool active = task < ntask;
+    const int pl = active ? task / Ky : 0, j = active ? task % Ky : 0;
+    double2 v[P];
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) v[n1] = active ? I[iidx(G, pl, t + T * n1, f, j)] : czero();
+    wfft_t1<NX, false>(v, t, xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF, G.twx);
+    double2* Ff = F + ((size_t)tl * 4 + f) * Kx;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int r = band_r(t1_pos<NX>(t, i), NX, G.kxm, Kx);
+      if (r >= 0) Ff[r] = v[i];
+    }
+  }
+  __syncthreads();
   const size_t KyKx = (size_t)Ky * Kx;
-  double2* slot = slots + (size_t)g * 3 * KyKx;
-
-  for (int r = t; r < Kx; r += T) {
-#pragma unroll
-    for (int f = 0; f < 3; ++f)
-      acc[f * Kx + r] = (active && !first_chunk) ? slot[f * KyKx + (size_t)j * Kx + r] : czero();
-  }
-  const size_t fstride = (size_t)Ky * NX;
-#pragma unroll 1
-  for (int pl = lo; pl < hi; ++pl) {
-    const double2* in = I + ((size_t)pl * 5 * Ky + j) * NX;
-#pragma unroll 1
-    for (int f = 0; f < 4; ++f) {
-      double2 v[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) v[m] = in[f * fstride + t + m * T];
-      fft_reg<NX, false>(v, t, sm, gid, G.twx);
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const int r = band_r(t + m * T, NX, G.kxm, Kx);
-        if (r >= 0) F[f * Kx + r] = v[m];
-      }
-    }
-    group_sync<NX>(gid);
-    const double s = ph.s[p0 + pl], w = ph.w[p0 + pl];
-    for (int r = t; r < Kx; r += T) {
-      const double kx = G.kxc[r];
-      const double2 fx = F[2 * Kx + r], fy = F[3 * Kx + r];
-      const double2 gx = cik(kx, fx), gy = cik(ky, fy);
-      C3 q = {F[r], F[Kx + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
-      q = expL(-s, q, G.ph, kx, ky, pr);
-      acc[r] = cadd(acc[r], cscale(w, q.u));
-      acc[Kx + r] = cadd(acc[Kx + r], cscale(w, q.v));
-      acc[2 * Kx + r] = cadd(acc[2 * Kx + r], cscale(w, q.e));
-    }
-    // F is rewritten by the next phase only after the next FFTs' barriers
-  }
-  if (active) {
-    for (int r = t; r < Kx; r += T) {
-#pragma unroll
-      for (int f = 0; f < 3; ++f) slot[f * KyKx + (size_t)j * Kx + r] = acc[f * Kx + r];
+  for (int idx = threadIdx.x; idx < GPW * Kx; idx += blockDim.x) {
+    const int tl = idx / Kx, r = idx % Kx;
+    const int task = blockIdx.x * GPW + tl;
+    if (task >= ntask) continue;
+    const int pl = task / Ky, j = task % Ky;
+    const double2* Ft = F + (size_t)tl * 4 * Kx;
+    const double kx = G.kxc[r], ky = G.kyc[j];
+    const double2 gx = cik(kx, Ft[2 * Kx + r]), gy = cik(ky, Ft[3 * Kx + r]);
+    C3 q = {Ft[r], Ft[Kx + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
+    q = expL(-ph.s[p0 + pl], q, G.ph, kx, ky, pr);
+    const double w = ph.w[p0 + pl];
+    double2* slot = slots + (size_t)pl * 3 * KyKx + (size_t)j * Kx + r;
+    if (first_chunk) {
+      slot[0] = cscale(w, q.u);
+      slot[KyKx] = cscale(w, q.v);
+      slot[2 * KyKx] = cscale(w, q.e);
+    } else {
+      slot[0] = cadd(slot[0], cscale(w, q.u));
+      slot[KyKx] = cadd(slot[KyKx], cscale(w, q.v));
+      slot[2 * KyKx] = cadd(slot[2 * KyKx], cscale(w, q.e));
     }
   }
 }

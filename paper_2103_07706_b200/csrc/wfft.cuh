@@ -1,0 +1,269 @@
+// Warp-level fp64 complex FFT, 16 points per lane (N = 16 * T, T <= 32).
+//
+// A transform of length N is owned by a group of T = N/16 lanes inside one
+// warp (32/T groups per warp), so every synchronisation is a __syncwarp.
+// Two-step (row/column) factorisation N = 16 x T:
+//
+//  type 1  in : lane t holds x[t + T*n1], n1 = 0..15      (register v[n1])
+//          16-point DFT in registers, twiddle W_N^{t k1}, ONE shared-memory
+//          transpose (real and imaginary halves in turn, so the buffer is
+//          16*S doubles), then the T-point DFTs over t:
+//            T <= 16: lane t' owns k1 = t' + T*c (c < 16/T), all k2 in regs;
+//            T == 32: lane t' = 2*k1 + h computes a 16-point DFT of the
+//                     h-decimated sequence and the final radix-2 stage is
+//                     a lane-pair exchange (__shfl_xor 1) -- no second
+//                     shared-memory round trip.
+//          out: see t1_pos() -- lane-owned positions k1 + 16*k2
+//  type 2  the transposed algorithm: input in the type-1 OUTPUT layout,
+//          output in the type-1 INPUT layout (lane t holds X[t + T*k2]).
+//
+// Pass B runs type 1 (spectral -> physical y), forms the quadratic products
+// on the positions it owns, and runs type 2 back without any reshuffle.
+// N = 8 is a single-lane DFT8 (both layouts natural).
+//
+// Twiddles: W_N^t from the global table (L1-resident), its powers by two
+// interleaved multiplication chains; W_16 and W_32 are compile-time constants.
+// Sign: FWD X[k] = sum x[n] e^{-2 pi i nk/N}; INV unnormalised e^{+...}.
+#pragma once
+#include "fft_reg.cuh"
+
+namespace pswe {
+
+template <int N>
+struct WF {
+  static constexpr int T = N >= 16 ? N / 16 : 1;   // lanes per transform
+  static constexpr int P = N >= 16 ? 16 : 8;       // points per lane
+  static constexpr int GPW = 32 / T;               // transforms per warp
+  static constexpr int S = T == 32 ? 34 : T + 1;   // transpose row stride (doubles)
+  // per-transform buffer in doubles; the padding staggers the groups that
+  // share a half-warp across distinct banks
+  static constexpr int PADD = T == 1 ? 1 : (T == 2 ? 2 : (T == 4 ? 4 : (T == 8 ? 8 : 0)));
+  static constexpr int XBUF = N >= 16 ? 16 * S + PADD : 2;
+};
+
+// cos/sin(2 pi e / 32), e = 0..7 (first octant + symmetry handled by caller)
+__device__ __forceinline__ double2 w32(int e, bool inv) {
+  // exact table of e^{+i 2 pi e/32} for e = 0..31, folded after unrolling
+  const double C[9] = {1.0,
+                       0.98078528040323044913,
+                       0.92387953251128675613,
+                       0.83146961230254523708,
+                       0.70710678118654752440,
+                       0.55557023301960222474,
+                       0.38268343236508977173,
+                       0.19509032201612826785,
+                       0.0};
+  e &= 31;
+  const int q = e >> 3, r = e & 7;
+  // angle = q*pi/2 + r*pi/16
+  double c = C[r], s = C[8 - r];
+  double re, im;
+  switch (q) {
+    case 0: re = c; im = s; break;
+    case 1: re = -s; im = c; break;
+    case 2: re = -c; im = -s; break;
+    default: re = s; im = -c; break;
+  }
+  return inv ? cmk(re, im) : cmk(re, -im);
+}
+__device__ __forceinline__ double2 w16(int e, bool inv) { return w32(2 * e, inv); }
+
+// natural-order 16-point DFT in registers: 4 x 4 Cooley-Tukey
+template <bool INV>
+__device__ __forceinline__ void dft16(double2* v) {
+  double2 a[4][4];  // a[n2][k1]
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) {
+    double2 y0 = v[n2], y1 = v[n2 + 4], y2 = v[n2 + 8], y3 = v[n2 + 12];
+    dft4<INV>(y0, y1, y2, y3);
+    a[n2][0] = y0;
+    a[n2][1] = y1;
+    a[n2][2] = y2;
+    a[n2][3] = y3;
+  }
+#pragma unroll
+  for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+    for (int k1 = 1; k1 < 4; ++k1) {
+      const int e = n2 * k1;
+      if (e == 4) {
+        a[n2][k1] = INV ? cmuli(a[n2][k1]) : cmk(a[n2][k1].y, -a[n2][k1].x);
+      } else {
+        a[n2][k1] = cmul(a[n2][k1], w16(e, INV));
+      }
+    }
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    double2 y0 = a[0][k1], y1 = a[1][k1], y2 = a[2][k1], y3 = a[3][k1];
+    dft4<INV>(y0, y1, y2, y3);
+    v[k1] = y0;
+    v[k1 + 4] = y1;
+    v[k1 + 8] = y2;
+    v[k1 + 12] = y3;
+  }
+}
+
+template <int L, bool INV>
+__device__ __forceinline__ void dftL(double2* v) {
+  if constexpr (L == 16) dft16<INV>(v);
+  else if constexpr (L == 8) dft8<INV>(v);
+  else if constexpr (L == 4) dft4<INV>(v[0], v[1], v[2], v[3]);
+  else if constexpr (L == 2) dft2<INV>(v[0], v[1]);
+}
+
+// v[k] *= w^k for k = 1..L-1 (two interleaved chains: odd and even powers)
+template <int L>
+__device__ __forceinline__ void apply_powers(double2* v, double2 w) {
+  if constexpr (L > 1) {
+    const double2 w2 = cmul(w, w);
+    double2 po = w, pe = w2;
+#pragma unroll
+    for (int k = 1; k < L; k += 2) {
+      v[k] = cmul(v[k], po);
+      po = cmul(po, w2);
+      if (k + 1 < L) {
+        v[k + 1] = cmul(v[k + 1], pe);
+        pe = cmul(pe, w2);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double2 twg(const double2* __restrict__ tw, int e, bool inv) {
+  double2 w = __ldg(tw + e);
+  if (inv) w.y = -w.y;
+  return w;
+}
+
+// position held in register i by lane t after a type-1 transform (== type-2 input)
+template <int N>
+__device__ __forceinline__ int t1_pos(int t, int i) {
+  constexpr int T = WF<N>::T;
+  if constexpr (N == 8) {
+    return i;
+  } else if constexpr (T <= 16) {
+    const int c = i / T, k2 = i % T;
+    return (t + T * c) + 16 * k2;
+  } else {
+    const int k1 = t >> 1, h = t & 1;
+    const int k2 = (i < 8) ? (8 * h + i) : (8 * h + (i - 8) + 16);
+    return k1 + 16 * k2;
+  }
+}
+
+// transpose helpers: write (re or im) of 16 values to rows k1 at column col,
+// read back a lane's values.  Each half is bracketed by __syncwarp.
+#define PSWE_XPOSE(WRITE_RE, WRITE_IM, READ_RE, READ_IM) \
+  __syncwarp();                                          \
+  _Pragma("unroll") WRITE_RE;                            \
+  __syncwarp();                                          \
+  _Pragma("unroll") READ_RE;                             \
+  __syncwarp();                                          \
+  _Pragma("unroll") WRITE_IM;                            \
+  __syncwarp();                                          \
+  _Pragma("unroll") READ_IM;
+
+// ---- type 1 -------------------------------------------------------------------
+// v[n1] = x[t + T n1] in; out per t1_pos.  xb: this transform's exchange buffer
+// (WF<N>::XBUF doubles); tw: global W_N^k table.
+template <int N, bool INV>
+__device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const double2* __restrict__ tw) {
+  if constexpr (N == 8) {
+    dft8<INV>(v);
+  } else {
+    constexpr int T = WF<N>::T, S = WF<N>::S;
+    dft16<INV>(v);
+    if constexpr (T > 1) {
+      apply_powers<16>(v, twg(tw, t, INV));
+      if constexpr (T <= 16) {
+        constexpr int C = 16 / T;
+        PSWE_XPOSE(
+            for (int k1 = 0; k1 < 16; ++k1) xb[k1 * S + t] = v[k1].x,
+            for (int k1 = 0; k1 < 16; ++k1) xb[k1 * S + t] = v[k1].y,
+            for (int c = 0; c < C; ++c) _Pragma("unroll") for (int n2 = 0; n2 < T; ++n2) v[c * T + n2].x = xb[(t + T * c) * S + n2],
+            for (int c = 0; c < C; ++c) _Pragma("unroll") for (int n2 = 0; n2 < T; ++n2) v[c * T + n2].y = xb[(t + T * c) * S + n2])
+#pragma unroll
+        for (int c = 0; c < C; ++c) dftL<T, INV>(v + c * T);
+      } else {
+        const int k1 = t >> 1, h = t & 1;
+        PSWE_XPOSE(
+            for (int q = 0; q < 16; ++q) xb[q * S + t] = v[q].x,
+            for (int q = 0; q < 16; ++q) xb[q * S + t] = v[q].y,
+            for (int m = 0; m < 16; ++m) v[m].x = xb[k1 * S + h + 2 * m],
+            for (int m = 0; m < 16; ++m) v[m].y = xb[k1 * S + h + 2 * m])
+        dft16<INV>(v);  // E_h[k2'], k2' = 0..15
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double2 send = h ? v[c] : v[8 + c];
+          double2 recv;
+          recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+          recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+          const double2 e0 = h ? recv : v[c];
+          const double2 e1 = h ? v[8 + c] : recv;
+          const double2 w = h ? w32(8 + c, INV) : w32(c, INV);  // W_32^{k2'}
+          const double2 we1 = cmul(w, e1);
+          v[c] = cadd(e0, we1);
+          v[8 + c] = csub(e0, we1);
+        }
+      }
+    }
+  }
+}
+
+// ---- type 2 -------------------------------------------------------------------
+// input in t1_pos layout; out v[k2] = X[t + T k2].
+template <int N, bool INV>
+__device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const double2* __restrict__ tw) {
+  if constexpr (N == 8) {
+    dft8<INV>(v);
+  } else {
+    constexpr int T = WF<N>::T, S = WF<N>::S;
+    if constexpr (T > 1) {
+      if constexpr (T <= 16) {
+        constexpr int C = 16 / T;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          dftL<T, INV>(v + c * T);                              // Z[n1][k1''], k1'' = 0..T-1
+          apply_powers<T>(v + c * T, twg(tw, t + T * c, INV));  // W_N^{n1 k1''}
+        }
+        PSWE_XPOSE(
+            for (int c = 0; c < C; ++c) _Pragma("unroll") for (int k = 0; k < T; ++k) xb[(t + T * c) * S + k] = v[c * T + k].x,
+            for (int c = 0; c < C; ++c) _Pragma("unroll") for (int k = 0; k < T; ++k) xb[(t + T * c) * S + k] = v[c * T + k].y,
+            for (int n1 = 0; n1 < 16; ++n1) v[n1].x = xb[n1 * S + t],
+            for (int n1 = 0; n1 < 16; ++n1) v[n1].y = xb[n1 * S + t])
+      } else {
+        const int n1 = t >> 1, h = t & 1;
+        // s_c = a + b, d_c = (a - b) W_32^c for this lane's c = 8h + cc
+        double2 q[16];
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const double2 a = v[cc], b = v[8 + cc];
+          const double2 sv = cadd(a, b);
+          const double2 dv = cmul(csub(a, b), h ? w32(8 + cc, INV) : w32(cc, INV));
+          const double2 send = h ? sv : dv;
+          double2 recv;
+          recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+          recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+          q[cc] = h ? recv : sv;
+          q[8 + cc] = h ? dv : recv;
+        }
+        dft16<INV>(q);  // Z[n1][2 q' + h]
+        // twiddle W_N^{n1 (2q'+h)} = W^{n1 h} (W^{2 n1})^{q'}
+        if (h) {
+          const double2 b1 = twg(tw, n1, INV);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) q[k] = cmul(q[k], b1);
+        }
+        apply_powers<16>(q, twg(tw, (2 * n1) & (N - 1), INV));
+        PSWE_XPOSE(
+            for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].x,
+            for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].y,
+            for (int m = 0; m < 16; ++m) v[m].x = xb[m * S + t],
+            for (int m = 0; m < 16; ++m) v[m].y = xb[m * S + t])
+      }
+    }
+    dft16<INV>(v);
+  }
+}
+
+}  // namespace pswe
