@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -169,7 +170,7 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
 template <int NY>
 int launchB(pswe_ctx* c, int np, cudaStream_t st) {
   using W = PassBW<NY>;
-  const size_t smem = W::bytes();
+  const size_t smem = W::bytes(c->Ky);
   auto kern = passB_kernel<NY>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
@@ -280,8 +281,6 @@ int check_nodes(const pswe_ctx* c) {
   }
   return PSWE_OK;
 }
-
-GridDev grid_of(const pswe_ctx* c) { return c->grid(); }
 
 int ensure_compact(pswe_ctx* c) {
   TRY(c->Uc.alloc(c->compact_elems()));

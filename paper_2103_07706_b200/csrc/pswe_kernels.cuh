@@ -20,6 +20,7 @@
 //                                   truncation, e^{-sL}, weighted ordered sum
 // followed by an ordered reduction over the phase-group slots.
 #pragma once
+#include "async_copy.cuh"
 #include "wfft.cuh"
 
 namespace pswe {
@@ -142,16 +143,19 @@ struct PassBW {
   static constexpr int T = WF<NY>::T, P = WF<NY>::P, GPW = WF<NY>::GPW;
   static constexpr int WARPS = 4;
   static constexpr int GPC = WARPS * GPW;  // rows per CTA
-  static size_t bytes() {
-    return (size_t)GPC * (WF<NY>::XBUF * sizeof(double) + (size_t)P * T * sizeof(double2));
+  // per warp: mbarrier | prefetch [GPW][2][Ky] | per group: xbuf, (u, v) stash
+  __host__ __device__ static size_t warp_bytes(int Ky) {
+    return 16 + (size_t)GPW * 2 * Ky * sizeof(double2) +
+           (size_t)GPW * (WF<NY>::XBUF * sizeof(double) + (size_t)P * T * sizeof(double2));
   }
+  static size_t bytes(int Ky) { return (size_t)WARPS * ((warp_bytes(Ky) + 15) / 16 * 16); }
 };
 
-// type-1 input of the packed pair A + iB at positions k = t + T n1
+// type-1 input of the packed pair A + iB at positions k = t + T n1, from the
+// prefetched half-spectra A = pre[0..Ky), B = pre[Ky..2Ky) (B absent: fb = 0)
 template <int NY>
-__device__ __forceinline__ void load_row_pair(double2* v, int t, const double2* row, int Ky, int kym, int fa,
-                                              int fb, int deriv_b, const double* __restrict__ kyc,
-                                              bool active) {
+__device__ __forceinline__ void build_pair(double2* v, int t, const double2* pre, int Ky, int kym, bool has_b,
+                                           bool deriv_b, const double* __restrict__ kyc) {
   constexpr int T = WF<NY>::T, P = WF<NY>::P;
 #pragma unroll
   for (int n1 = 0; n1 < P; ++n1) {
@@ -159,7 +163,6 @@ __device__ __forceinline__ void load_row_pair(double2* v, int t, const double2* 
     int jj;
     bool cj;
     v[n1] = czero();
-    if (!active) continue;
     if (k <= kym) {
       jj = k;
       cj = false;
@@ -169,10 +172,10 @@ __device__ __forceinline__ void load_row_pair(double2* v, int t, const double2* 
     } else {
       continue;
     }
-    const double2 A = row[fa * Ky + jj];
+    const double2 A = pre[jj];
     double2 B = czero();
-    if (fb >= 0) {
-      B = row[fb * Ky + jj];
+    if (has_b) {
+      B = pre[Ky + jj];
       if (deriv_b) B = cik(__ldg(kyc + jj), B);
     }
     if (jj == 0) {
@@ -214,59 +217,106 @@ __device__ __forceinline__ void unpack_store(const double2* v, int t, double2* o
   }
 }
 
+// transform `it` of a row: inputs (fa, fb) of the packed pair
+//   0: (u, v)   1: (ux, i ky u)   2: (vx, i ky v)   3: (depth, -)
+__device__ __forceinline__ int passB_fa(int it) { return it == 0 ? 0 : (it == 1 ? 3 : (it == 2 ? 4 : 2)); }
+__device__ __forceinline__ int passB_fb(int it) { return it == 0 ? 1 : (it == 1 ? 0 : (it == 2 ? 1 : -1)); }
+
+// lane 0 of the warp queues the bulk copies of transform `it`'s inputs for the
+// warp's GPW rows into its prefetch buffer
+template <int NY>
+__device__ __forceinline__ void passB_prefetch(int it, int lane, double2* pre, uint64_t* bar,
+                                               const double2* __restrict__ I, int first_task, int ntask,
+                                               int Ky) {
+  constexpr int GPW = WF<NY>::GPW;
+  if (lane == 0) {
+    const int fa = passB_fa(it), fb = passB_fb(it);
+    const uint32_t seg = (uint32_t)Ky * sizeof(double2);
+    uint32_t bytes = 0;
+    for (int g = 0; g < GPW; ++g) {
+      const int task = first_task + g;
+      if (task >= ntask) break;
+      bytes += fb >= 0 ? 2 * seg : seg;
+    }
+    mbar_arrive_expect_tx(bar, bytes);
+    for (int g = 0; g < GPW; ++g) {
+      const int task = first_task + g;
+      if (task >= ntask) break;
+      const double2* row = I + (size_t)task * 5 * Ky;
+      bulk_g2s(pre + (size_t)g * 2 * Ky, row + (size_t)fa * Ky, seg, bar);
+      if (fb >= 0) bulk_g2s(pre + (size_t)g * 2 * Ky + Ky, row + (size_t)fb * Ky, seg, bar);
+    }
+  }
+}
+
 template <int NY>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     passB_kernel(GridDev Gd, int np, double2* __restrict__ I) {
   using W = PassBW<NY>;
-  constexpr int T = W::T, P = W::P;
-  extern __shared__ double2 dsm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = lane % T;
-  const int group = warp * W::GPW + lane / T;
-  double2* uv = dsm + (size_t)group * P * T;  // [P][T] physical (u, v) at this lane's positions
-  double* xb = reinterpret_cast<double*>(dsm + (size_t)W::GPC * P * T) + (size_t)group * WF<NY>::XBUF;
+  constexpr int T = W::T, P = W::P, GPW = W::GPW;
+  extern __shared__ __align__(16) unsigned char sbytes[];
   const int Ky = Gd.Ky;
-  const int task = blockIdx.x * W::GPC + group;
-  const bool active = task < np * Gd.nx;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane % T, g = lane / T;
+  unsigned char* wbase = sbytes + (size_t)warp * ((W::warp_bytes(Ky) + 15) / 16 * 16);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wbase);
+  double2* pre = reinterpret_cast<double2*>(wbase + 16);             // [GPW][2][Ky]
+  double* xb = reinterpret_cast<double*>(pre + (size_t)GPW * 2 * Ky) + (size_t)g * WF<NY>::XBUF;
+  double2* uv = reinterpret_cast<double2*>(reinterpret_cast<double*>(pre + (size_t)GPW * 2 * Ky) +
+                                           (size_t)GPW * WF<NY>::XBUF) +
+                (size_t)g * P * T;                                      // [P][T]
+  const int ntask = np * Gd.nx;
+  const int first_task = (blockIdx.x * W::WARPS + warp) * GPW;
+  const int task = first_task + g;
+  const bool active = task < ntask;
   double2* row = I + (size_t)(active ? task : 0) * 5 * Ky;
+  const double2* mypre = pre + (size_t)g * 2 * Ky;
+
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  passB_prefetch<NY>(0, lane, pre, bar, I, first_task, ntask, Ky);
 
   double2 v[P];
   double pa[P];
-  // (u, v)
-  load_row_pair<NY>(v, t, row, Ky, Gd.kym, 0, 1, 0, Gd.kyc, active);
-  wfft_t1<NY, true>(v, t, xb, Gd.twy);
+#pragma unroll 1
+  for (int it = 0; it < 4; ++it) {
+    mbar_wait(bar, it & 1);
+    build_pair<NY>(v, t, mypre, Ky, Gd.kym, it < 3, it == 1 || it == 2, Gd.kyc);
+    __syncwarp();  // prefetch buffer consumed
+    // queue the next transform's inputs; they land while this one computes.
+    // (No `continue` in this loop: nvcc 12.9 mis-carried pa[] across one.)
+    if (it < 3) passB_prefetch<NY>(it + 1, lane, pre, bar, I, first_task, ntask, Ky);
+    wfft_t1<NY, true>(v, t, xb, Gd.twy);
+    if (it == 0) {
 #pragma unroll
-  for (int i = 0; i < P; ++i) uv[i * T + t] = v[i];
-  // (ux, uy): A = -(u ux + v uy)
-  load_row_pair<NY>(v, t, row, Ky, Gd.kym, 3, 0, 1, Gd.kyc, active);
-  wfft_t1<NY, true>(v, t, xb, Gd.twy);
+      for (int i = 0; i < P; ++i) uv[i * T + t] = v[i];
+    } else if (it == 1) {
 #pragma unroll
-  for (int i = 0; i < P; ++i) {
-    const double2 q = uv[i * T + t];
-    pa[i] = -(q.x * v[i].x + q.y * v[i].y);
+      for (int i = 0; i < P; ++i) {
+        const double2 q = uv[i * T + t];
+        pa[i] = -(q.x * v[i].x + q.y * v[i].y);  // A = -(u ux + v uy)
+      }
+    } else if (it == 2) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const double2 q = uv[i * T + t];
+        v[i] = cmk(pa[i], -(q.x * v[i].x + q.y * v[i].y));  // A + iB, B = -(u vx + v vy)
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const double2 q = uv[i * T + t];
+        v[i] = cmk(q.x * v[i].x, q.y * v[i].x);  // C + iD = u depth + i v depth
+      }
+    }
+    if (it < 2) continue;
+    wfft_t2<NY, false>(v, t, xb, Gd.twy);
+    const int fo = it == 2 ? 0 : 2;
+    unpack_store<NY>(v, t, row + (size_t)fo * Ky, row + (size_t)(fo + 1) * Ky, Ky, active);
   }
-  // (vx, vy): B = -(u vx + v vy)
-  load_row_pair<NY>(v, t, row, Ky, Gd.kym, 4, 1, 1, Gd.kyc, active);
-  wfft_t1<NY, true>(v, t, xb, Gd.twy);
-#pragma unroll
-  for (int i = 0; i < P; ++i) {
-    const double2 q = uv[i * T + t];
-    v[i] = cmk(pa[i], -(q.x * v[i].x + q.y * v[i].y));
-  }
-  wfft_t2<NY, false>(v, t, xb, Gd.twy);
-  __syncwarp();  // every lane of the group has read fields 0..4 it needs from row
-  unpack_store<NY>(v, t, row, row + Ky, Ky, active);
-  // (depth, 0): C = u depth, D = v depth
-  load_row_pair<NY>(v, t, row, Ky, Gd.kym, 2, -1, 0, Gd.kyc, active);
-  wfft_t1<NY, true>(v, t, xb, Gd.twy);
-#pragma unroll
-  for (int i = 0; i < P; ++i) {
-    const double2 q = uv[i * T + t];
-    v[i] = cmk(q.x * v[i].x, q.y * v[i].x);
-  }
-  wfft_t2<NY, false>(v, t, xb, Gd.twy);
-  __syncwarp();
-  unpack_store<NY>(v, t, row + 2 * Ky, row + 3 * Ky, Ky, active);
 }
 
 // ============================================================================
