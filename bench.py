@@ -251,6 +251,8 @@ def run_ours(args, ws, rank, local):
     ctx = pk.dynamics.context(case.state, case.params)
     ctx.set_propagator("exact")
     ctx.set_quadrature(case.quadrature.s, case.quadrature.w)
+    if args.chunk_mb:
+        ctx.set_chunk_bytes(int(args.chunk_mb * (1 << 20)))
     U = pk.dynamics.upload(ctx, case.state)
     Uc = ctx.pack(U)
     Ac = ctx.empty_compact()
@@ -365,6 +367,8 @@ def run_sweep(pk, cases, torch, flush, stream, steps=3):
     for r in (4, 5, 6, 7):
         for M in (8, 32, 128, 256):
             c = cases.case_c5(r, M)
+            if os.environ.get("PSWE_BENCH_VERBOSE"):
+                print(f"sweep point r={r} M={M}", file=sys.stderr, flush=True)
             ctx = pk.dynamics.context(c.state, c.params)
             ctx.set_propagator("exact")
             ctx.set_quadrature(c.quadrature.s, c.quadrature.w)
@@ -409,6 +413,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--chunk-mb", type=float, default=0.0, help="L2-resident chunk size (default: library's)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)

@@ -89,8 +89,9 @@ struct pswe_ctx {
   double Lambda = 0;
   DevBuf<double> a_dev;
   // scratch
-  size_t chunk_bytes = size_t(40) << 20;
+  size_t chunk_bytes = size_t(160) << 20;
   DevBuf<double2> inter, slots, Uc, Ac, Ac2;
+  double2* inter2 = nullptr;  // I2 region inside `inter`, after the CP phases of I1
   DevBuf<double2> full_tmp;  // stepper: edt, u1, u2 (3 states) + run ping-pong (2 states)
   DevBuf<int> flags;
   int* flags_host = nullptr;
@@ -175,21 +176,30 @@ int launchB(pswe_ctx* c, int np, cudaStream_t st) {
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, c->inter.p);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, c->inter.p, c->inter2);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
 
 template <int NX>
-int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int first, cudaStream_t st) {
+int pass_c_groups(const pswe_ctx* c, int CP) {
+  // enough CTAs for ~4 per SM, each looping over CP/Gc phases
+  const int cols = (c->Ky + PassCW<NX>::GPW - 1) / PassCW<NX>::GPW;
+  const int want = (4 * 148 + cols - 1) / cols;
+  return std::max(1, std::min(want, CP));
+}
+
+template <int NX>
+int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, cudaStream_t st) {
   using W = PassCW<NX>;
   const size_t smem = W::bytes(c->Kx);
   auto kern = passC_kernel<NX>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int blocks = (np * c->Ky + W::GPW - 1) / W::GPW;
+  const int cols = (c->Ky + W::GPW - 1) / W::GPW;
+  const int blocks = cols * Gc;
   ProfScope ps(c, 2, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, c->inter.p, c->slots.p, first);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, c->inter2, c->slots.p, first);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -219,15 +229,27 @@ int dispatchB(pswe_ctx* c, int np, cudaStream_t st) {
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported ny = %d", c->ny);
 }
-int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int first, cudaStream_t st) {
+int groupsC(const pswe_ctx* c, int CP) {
   switch (c->nx) {
-    case 8: return launchC<8>(c, ph, p0, np, first, st);
-    case 16: return launchC<16>(c, ph, p0, np, first, st);
-    case 32: return launchC<32>(c, ph, p0, np, first, st);
-    case 64: return launchC<64>(c, ph, p0, np, first, st);
-    case 128: return launchC<128>(c, ph, p0, np, first, st);
-    case 256: return launchC<256>(c, ph, p0, np, first, st);
-    case 512: return launchC<512>(c, ph, p0, np, first, st);
+    case 8: return pass_c_groups<8>(c, CP);
+    case 16: return pass_c_groups<16>(c, CP);
+    case 32: return pass_c_groups<32>(c, CP);
+    case 64: return pass_c_groups<64>(c, CP);
+    case 128: return pass_c_groups<128>(c, CP);
+    case 256: return pass_c_groups<256>(c, CP);
+    default: return pass_c_groups<512>(c, CP);
+  }
+}
+
+int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, cudaStream_t st) {
+  switch (c->nx) {
+    case 8: return launchC<8>(c, ph, p0, np, Gc, first, st);
+    case 16: return launchC<16>(c, ph, p0, np, Gc, first, st);
+    case 32: return launchC<32>(c, ph, p0, np, Gc, first, st);
+    case 64: return launchC<64>(c, ph, p0, np, Gc, first, st);
+    case 128: return launchC<128>(c, ph, p0, np, Gc, first, st);
+    case 256: return launchC<256>(c, ph, p0, np, Gc, first, st);
+    case 512: return launchC<512>(c, ph, p0, np, Gc, first, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
@@ -236,18 +258,19 @@ int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int first, cudaSt
 // then the ordered slot reduction.  `P` live phases in (s, w) device arrays.
 int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const double2* Uc, double2* Ac,
                 cudaStream_t st) {
-  const size_t per_phase = (size_t)5 * c->Ky * c->nx;  // double2 elements
+  const size_t per_phase = (size_t)9 * c->Ky * c->nx;  // I1 (5 fields) + I2 (4 fields), double2
   int CP = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
   CP = std::min(CP, P);
-  const int Gc = CP;  // one accumulation slot per phase position in a chunk
+  const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
   TRY(c->inter.alloc(per_phase * CP));
+  c->inter2 = c->inter.p + (size_t)5 * c->Ky * c->nx * CP;
   TRY(c->slots.alloc((size_t)Gc * c->compact_elems()));
   PhaseDev ph{s, w, P};
   for (int p0 = 0; p0 < P; p0 += CP) {
     const int np = std::min(CP, P - p0);
     TRY(dispatchA(c, ph, p0, np, Uc, st));
     TRY(dispatchB(c, np, st));
-    TRY(dispatchC(c, ph, p0, np, p0 == 0 ? 1 : 0, st));
+    TRY(dispatchC(c, ph, p0, np, Gc, p0 == 0 ? 1 : 0, st));
   }
   const size_t n = c->compact_elems();
   ProfScope ps(c, 3, st);

@@ -8,9 +8,11 @@
 //             r = compact kx index 0..Kx-1 (wx = r for r <= KXM, r - Kx after).
 //             Only the 2/3 band |wx| <= nx/3, |wy| <= ny/3 (grid.py:102-103)
 //             is stored; the ky < 0 half is the conjugate mirror.
-//   I (chunk intermediates): I[p][x][f][j], p = phase in chunk, x = 0..nx-1
+//   I1 (pass A -> B): I1[p][x][f][j], p = phase in chunk, x = 0..nx-1
 //             (physical x), f in 0..4, j = 0..KYM (spectral y): one physical
 //             row's five half-spectra are contiguous for pass B.
+//   I2 (pass B -> C): I2[p][f][j][x], f in 0..3: one ky column contiguous
+//             for pass C.  Strided accesses are only ever stores (A, B).
 //
 // Averaged RHS (averaging.py:116-156) for a chunk of phases:
 //   pass A  (per phase, ky column)  e^{sL} per mode + 5 inverse x-FFTs
@@ -193,7 +195,7 @@ __device__ __forceinline__ void build_pair(double2* v, int t, const double2* pre
 // for j = 0..Ky-1 and store them.
 template <int NY>
 __device__ __forceinline__ void unpack_store(const double2* v, int t, double2* outX, double2* outY, int Ky,
-                                             bool active) {
+                                             int stride, bool active) {
   constexpr int T = WF<NY>::T, P = WF<NY>::P;
   constexpr int MU = (NY / 3 + 1 + T - 1) / T;
 #pragma unroll
@@ -211,8 +213,8 @@ __device__ __forceinline__ void unpack_store(const double2* v, int t, double2* o
     }
     if (active && j < Ky) {
       const double2 a = v[m];
-      outX[j] = cmk(0.5 * (a.x + zm.x), 0.5 * (a.y - zm.y));
-      outY[j] = cmk(0.5 * (a.y + zm.y), -0.5 * (a.x - zm.x));
+      outX[(size_t)j * stride] = cmk(0.5 * (a.x + zm.x), 0.5 * (a.y - zm.y));
+      outY[(size_t)j * stride] = cmk(0.5 * (a.y + zm.y), -0.5 * (a.x - zm.x));
     }
   }
 }
@@ -251,7 +253,7 @@ __device__ __forceinline__ void passB_prefetch(int it, int lane, double2* pre, u
 
 template <int NY>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
-    passB_kernel(GridDev Gd, int np, double2* __restrict__ I) {
+    passB_kernel(GridDev Gd, int np, const double2* __restrict__ I, double2* __restrict__ I2) {
   using W = PassBW<NY>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW;
   extern __shared__ __align__(16) unsigned char sbytes[];
@@ -269,7 +271,9 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   const int first_task = (blockIdx.x * W::WARPS + warp) * GPW;
   const int task = first_task + g;
   const bool active = task < ntask;
-  double2* row = I + (size_t)(active ? task : 0) * 5 * Ky;
+  const int pl = active ? task / Gd.nx : 0, x = active ? task % Gd.nx : 0;
+  const size_t KyNX = (size_t)Ky * Gd.nx;
+  double2* out = I2 + (size_t)pl * 4 * KyNX + x;  // I2[pl][f][j][x]
   const double2* mypre = pre + (size_t)g * 2 * Ky;
 
   if (lane == 0) {
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     if (it < 2) continue;
     wfft_t2<NY, false>(v, t, xb, Gd.twy);
     const int fo = it == 2 ? 0 : 2;
-    unpack_store<NY>(v, t, row + (size_t)fo * Ky, row + (size_t)(fo + 1) * Ky, Ky, active);
+    unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
   }
 }
 
@@ -330,61 +334,105 @@ template <int NX>
 struct PassCW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 4;
+  static constexpr int CPT = 3;  // combine modes per thread (GPW * Kx <= 3 * 128)
+  // 2 mbarriers | prefetch [4][GPW][NX] | F [GPW][4][Kx] | xbuf per group
   static size_t bytes(int Kx) {
-    return (size_t)GPW * 4 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
+    return 16 + (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * 4 * Kx * sizeof(double2) +
+           (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
   }
 };
 
+// CTA = (GPW ky columns) x (phase group g of the chunk).  Loops over the
+// group's phases in ascending order; each phase's 4 product columns
+// (contiguous in I2) are TMA-bulk-prefetched while the previous phase
+// computes.  Warp f transforms field f; then every thread combines its modes
+// (flux divergence, e^{-sL}, weight) into register accumulators, which are
+// added to the group's slot once at the end (slot values from earlier chunks
+// are read after the loop).
 template <int NX>
-__global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
-    passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, const double2* __restrict__ I,
+__global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
+    passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
                  double2* __restrict__ slots, int first_chunk) {
   using W = PassCW<NX>;
-  constexpr int T = W::T, P = W::P, GPW = W::GPW;
-  extern __shared__ double2 dsm[];
+  constexpr int T = W::T, P = W::P, GPW = W::GPW, CPT = W::CPT;
+  extern __shared__ __align__(16) unsigned char sbytes[];
   const int Kx = G.Kx, Ky = G.Ky;
-  double2* F = dsm;  // [GPW][4][Kx]
-  double* xbuf = reinterpret_cast<double*>(dsm + (size_t)GPW * 4 * Kx);
-  const int ntask = np * Ky;
-  {
-    const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;
-    const int tl = lane / T, t = lane % T;
-    const int task = blockIdx.x * GPW + tl;
-    const bool active = task < ntask;
-    const int pl = active ? task / Ky : 0, j = active ? task % Ky : 0;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
+  double2* pre = reinterpret_cast<double2*>(sbytes + 16);  // [4][GPW][NX]
+  double2* F = pre + (size_t)4 * GPW * NX;                  // [GPW][4][Kx]
+  double* xbuf = reinterpret_cast<double*>(F + (size_t)GPW * 4 * Kx);
+  const int cols = (Ky + GPW - 1) / GPW;
+  const int cb = blockIdx.x % cols, g = blockIdx.x / cols;
+  const int lo = (int)(((long long)g * np) / Gc), hi = (int)(((long long)(g + 1) * np) / Gc);
+  const size_t KyKx = (size_t)Ky * Kx, KyNX = (size_t)Ky * NX;
+  const int j0 = cb * GPW;
+  const int ncol = min(GPW, Ky - j0);  // active columns of this CTA (contiguous in I2)
+
+  auto prefetch = [&](int pl) {
+    // fields f: the CTA's ncol columns are contiguous: I2[pl][f][j0 .. j0+ncol)[x]
+    const uint32_t seg = (uint32_t)(ncol * NX * sizeof(double2));
+    mbar_arrive_expect_tx(bar, 4 * seg);
+    for (int f = 0; f < 4; ++f)
+      bulk_g2s(pre + (size_t)f * GPW * NX, I2 + ((size_t)pl * 4 + f) * KyNX + (size_t)j0 * NX, seg, bar);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    if (lo < hi) prefetch(lo);
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;
+  const int tl = lane / T, t = lane % T;
+  double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
+  double2* Ff = F + ((size_t)tl * 4 + f) * Kx;
+  const double2* mine = pre + ((size_t)f * GPW + tl) * NX;
+  C3 acc[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) acc[c] = c3zero();
+#pragma unroll 1
+  for (int pl = lo; pl < hi; ++pl) {
+    mbar_wait(bar, (pl - lo) & 1);
     double2 v[P];
 #pragma unroll
-    for (int n1 = 0; n1 < P; ++n1) v[n1] = active ? I[iidx(G, pl, t + T * n1, f, j)] : czero();
-    wfft_t1<NX, false>(v, t, xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF, G.twx);
-    double2* Ff = F + ((size_t)tl * 4 + f) * Kx;
+    for (int n1 = 0; n1 < P; ++n1) v[n1] = mine[t + T * n1];
+    __syncthreads();  // prefetch buffer consumed; F free (previous combine done)
+    if (threadIdx.x == 0 && pl + 1 < hi) prefetch(pl + 1);
+    wfft_t1<NX, false>(v, t, xb, G.twx);
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       const int r = band_r(t1_pos<NX>(t, i), NX, G.kxm, Kx);
       if (r >= 0) Ff[r] = v[i];
     }
+    __syncthreads();
+    const double s = ph.s[p0 + pl], w = ph.w[p0 + pl];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int idx = threadIdx.x + c * W::WARPS * 32;
+      const int tt = idx / Kx, r = idx % Kx;
+      if (tt < ncol) {
+        const double2* Ft = F + (size_t)tt * 4 * Kx;
+        const double kx = G.kxc[r], ky = G.kyc[j0 + tt];
+        const double2 gx = cik(kx, Ft[2 * Kx + r]), gy = cik(ky, Ft[3 * Kx + r]);
+        C3 q = {Ft[r], Ft[Kx + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
+        q = expL(-s, q, G.ph, kx, ky, pr);
+        acc[c] = c3add(acc[c], c3scale(w, q));
+      }
+    }
   }
-  __syncthreads();
-  const size_t KyKx = (size_t)Ky * Kx;
-  for (int idx = threadIdx.x; idx < GPW * Kx; idx += blockDim.x) {
-    const int tl = idx / Kx, r = idx % Kx;
-    const int task = blockIdx.x * GPW + tl;
-    if (task >= ntask) continue;
-    const int pl = task / Ky, j = task % Ky;
-    const double2* Ft = F + (size_t)tl * 4 * Kx;
-    const double kx = G.kxc[r], ky = G.kyc[j];
-    const double2 gx = cik(kx, Ft[2 * Kx + r]), gy = cik(ky, Ft[3 * Kx + r]);
-    C3 q = {Ft[r], Ft[Kx + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
-    q = expL(-ph.s[p0 + pl], q, G.ph, kx, ky, pr);
-    const double w = ph.w[p0 + pl];
-    double2* slot = slots + (size_t)pl * 3 * KyKx + (size_t)j * Kx + r;
-    if (first_chunk) {
-      slot[0] = cscale(w, q.u);
-      slot[KyKx] = cscale(w, q.v);
-      slot[2 * KyKx] = cscale(w, q.e);
-    } else {
-      slot[0] = cadd(slot[0], cscale(w, q.u));
-      slot[KyKx] = cadd(slot[KyKx], cscale(w, q.v));
-      slot[2 * KyKx] = cadd(slot[2 * KyKx], cscale(w, q.e));
+  // slot (+)= this group's phases, in chunk order
+  double2* slot = slots + (size_t)g * 3 * KyKx;
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int idx = threadIdx.x + c * W::WARPS * 32;
+    const int tt = idx / Kx, r = idx % Kx;
+    if (tt < ncol) {
+      double2* sp = slot + (size_t)(j0 + tt) * Kx + r;
+      C3 a = acc[c];
+      if (!first_chunk) a = c3add({sp[0], sp[KyKx], sp[2 * KyKx]}, a);
+      sp[0] = a.u;
+      sp[KyKx] = a.v;
+      sp[2 * KyKx] = a.e;
     }
   }
 }
