@@ -109,7 +109,9 @@ struct pswe_ctx {
     G.ph = Phys{f, g, H};
     G.inv_n2 = 1.0 / ((double)nx * (double)ny);
     G.kxc = kxc.p; G.kyc = kyc.p; G.kxf = kxf.p; G.kyf = kyf.p;
-    G.twx = twx.p; G.twy = twy.p; G.bc = bc.p;
+    G.twx = WTab{twx.p, twx.p + nx, twx.p + nx + 16 * ((nx >= 16) ? nx / 16 : 1)};
+    G.twy = WTab{twy.p, twy.p + ny, twy.p + ny + 16 * ((ny >= 16) ? ny / 16 : 1)};
+    G.bc = bc.p;
     return G;
   }
   Prop prop() const { return Prop{kind, n_poly, Lambda, a_dev.p}; }
@@ -426,13 +428,16 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
     pswe_destroy(c);
     return rc;
   }
-  if ((rc = c->twx.alloc(nx)) || (rc = c->twy.alloc(ny)) || (rc = c->bc.alloc((size_t)c->Ky * c->Kx)) ||
+  const int Tx = nx >= 16 ? nx / 16 : 1, Ty = ny >= 16 ? ny / 16 : 1;
+  if ((rc = c->twx.alloc(nx + 32 * Tx)) || (rc = c->twy.alloc(ny + 32 * Ty)) || (rc = c->bc.alloc((size_t)c->Ky * c->Kx)) ||
       (rc = c->flags.alloc(1))) {
     pswe_destroy(c);
     return rc;
   }
   twiddle_kernel<<<(nx + 255) / 256, 256>>>(c->twx.p, nx);
   twiddle_kernel<<<(ny + 255) / 256, 256>>>(c->twy.p, ny);
+  wtab_init_kernel<<<1, 256>>>(nx, c->twx.p + nx, c->twx.p + nx + 16 * Tx);
+  wtab_init_kernel<<<1, 256>>>(ny, c->twy.p + ny, c->twy.p + ny + 16 * Ty);
   cudaMemset(c->bc.p, 0, (size_t)c->Ky * c->Kx * sizeof(double2));
   cudaMemset(c->flags.p, 0, sizeof(int));
   {

@@ -35,8 +35,8 @@ struct GridDev {
   const double* kyc;   // [Ky]  ky >= 0
   const double* kxf;   // [nx]  full kx (fft order)
   const double* kyf;   // [ny]
-  const double2* twx;  // [nx]  exp(-2 pi i k/nx)
-  const double2* twy;  // [ny]
+  WTab twx;            // per-lane FFT twiddle tables, length nx
+  WTab twy;            // length ny
   const double2* bc;   // [Ky][Kx] compact (Hermitian-projected) topography
 };
 
@@ -150,44 +150,61 @@ struct PassBW {
     return 16 + (size_t)GPW * 2 * Ky * sizeof(double2) +
            (size_t)GPW * (WF<NY>::XBUF * sizeof(double) + (size_t)P * T * sizeof(double2));
   }
-  static size_t bytes(int Ky) { return (size_t)WARPS * ((warp_bytes(Ky) + 15) / 16 * 16); }
+  static size_t bytes(int Ky) { return (size_t)WARPS * ((warp_bytes(Ky) + 15) / 16 * 16) + (size_t)Ky * sizeof(double); }
 };
 
-// type-1 input of the packed pair A + iB at positions k = t + T n1, from the
-// prefetched half-spectra A = pre[0..Ky), B = pre[Ky..2Ky) (B absent: fb = 0)
-template <int NY>
-__device__ __forceinline__ void build_pair(double2* v, int t, const double2* pre, int Ky, int kym, bool has_b,
-                                           bool deriv_b, const double* __restrict__ kyc) {
-  constexpr int T = WF<NY>::T, P = WF<NY>::P;
-#pragma unroll
-  for (int n1 = 0; n1 < P; ++n1) {
-    const int k = t + T * n1;
-    int jj;
-    bool cj;
-    v[n1] = czero();
-    if (k <= kym) {
-      jj = k;
-      cj = false;
-    } else if (k >= NY - kym) {
-      jj = NY - k;
-      cj = true;
+// type-1 input of the packed pair A + iB at position k = t + T*N1, from the
+// prefetched half-spectra A = pre[0..Ky), B = pre[Ky..2Ky).  The band tests
+// are resolved at compile time except for the (at most two) register slots
+// whose k range straddles a band edge.
+template <int NY, int N1, bool HAS_B, bool DERIV>
+__device__ __forceinline__ double2 pair_val(int t, const double2* pre, const double* kys) {
+  constexpr int T = WF<NY>::T, KYM = NY / 3, Ky = KYM + 1;
+  constexpr int kmin = T * N1, kmax = T * N1 + T - 1;
+  if constexpr (kmin > KYM && kmax < NY - KYM) {
+    return czero();
+  } else {
+    const int k = t + kmin;
+    bool lo;
+    if constexpr (kmax <= KYM) {
+      lo = true;
+    } else if constexpr (kmin >= NY - KYM) {
+      lo = false;
     } else {
-      continue;
+      lo = k <= KYM;
+      if (!lo && k < NY - KYM) return czero();
     }
+    const int jj = lo ? k : NY - k;
     const double2 A = pre[jj];
     double2 B = czero();
-    if (has_b) {
+    if constexpr (HAS_B) {
       B = pre[Ky + jj];
-      if (deriv_b) B = cik(__ldg(kyc + jj), B);
+      if constexpr (DERIV) B = cik(kys[jj], B);
     }
-    if (jj == 0) {
-      v[n1] = cmk(A.x, B.x);  // Hermitian projection of the y-mean bin
-    } else if (!cj) {
-      v[n1] = cmk(A.x - B.y, A.y + B.x);
-    } else {
-      v[n1] = cmk(A.x + B.y, B.x - A.y);
+    if constexpr (N1 == 0) {
+      if (t == 0) return cmk(A.x, B.x);  // Hermitian projection of the y-mean bin
     }
+    return lo ? cmk(A.x - B.y, A.y + B.x) : cmk(A.x + B.y, B.x - A.y);
   }
+}
+
+template <int NY, bool HAS_B, bool DERIV, int N1 = 0>
+__device__ __forceinline__ void build_pair_t(double2* v, int t, const double2* pre, const double* kys) {
+  if constexpr (N1 < WF<NY>::P) {
+    v[N1] = pair_val<NY, N1, HAS_B, DERIV>(t, pre, kys);
+    build_pair_t<NY, HAS_B, DERIV, N1 + 1>(v, t, pre, kys);
+  }
+}
+
+// it: 0 (u, v), 1 (ux, i ky u), 2 (vx, i ky v), 3 (depth, -)
+template <int NY>
+__device__ __forceinline__ void build_pair(double2* v, int t, const double2* pre, const double* kys, int it) {
+  if (it == 0)
+    build_pair_t<NY, true, false>(v, t, pre, kys);
+  else if (it < 3)
+    build_pair_t<NY, true, true>(v, t, pre, kys);
+  else
+    build_pair_t<NY, false, false>(v, t, pre, kys);
 }
 
 // after a type-2 forward transform (v[k2] = Z[t + T k2]): split the packed pair
@@ -275,12 +292,14 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   const size_t KyNX = (size_t)Ky * Gd.nx;
   double2* out = I2 + (size_t)pl * 4 * KyNX + x;  // I2[pl][f][j][x]
   const double2* mypre = pre + (size_t)g * 2 * Ky;
+  double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * ((W::warp_bytes(Ky) + 15) / 16 * 16));
+  for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
 
   if (lane == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  __syncwarp();
+  __syncthreads();
   passB_prefetch<NY>(0, lane, pre, bar, I, first_task, ntask, Ky);
 
   double2 v[P];
@@ -288,7 +307,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
 #pragma unroll 1
   for (int it = 0; it < 4; ++it) {
     mbar_wait(bar, it & 1);
-    build_pair<NY>(v, t, mypre, Ky, Gd.kym, it < 3, it == 1 || it == 2, Gd.kyc);
+    build_pair<NY>(v, t, mypre, kys, it);
     __syncwarp();  // prefetch buffer consumed
     // queue the next transform's inputs; they land while this one computes.
     // (No `continue` in this loop: nvcc 12.9 mis-carried pa[] across one.)

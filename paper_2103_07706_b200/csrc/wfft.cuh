@@ -21,8 +21,8 @@
 // on the positions it owns, and runs type 2 back without any reshuffle.
 // N = 8 is a single-lane DFT8 (both layouts natural).
 //
-// Twiddles: W_N^t from the global table (L1-resident), its powers by two
-// interleaved multiplication chains; W_16 and W_32 are compile-time constants.
+// Twiddles: per-lane tables (WTab, global, L1-resident, loads independent of
+// the data so they issue early); W_16 and W_32 are compile-time constants.
 // Sign: FWD X[k] = sum x[n] e^{-2 pi i nk/N}; INV unnormalised e^{+...}.
 #pragma once
 #include "fft_reg.cuh"
@@ -129,6 +129,17 @@ __device__ __forceinline__ void apply_powers(double2* v, double2 w) {
   }
 }
 
+// twiddle tables of one transform length N.  t0 is what the FFT reads; the
+// per-lane tables t1/t2 (16*T entries each, kept for experiments) were slower
+// in pass B, where shared memory leaves L1 too small to hold them:
+//   t1[k1*T + t] = W_N^{t k1}                      (type 1, after the first DFT16)
+//   t2[i*T + t]  = type-2 twiddle of register i of lane t
+struct WTab {
+  const double2* t0;  // W_N^k, k = 0..N-1 (powers are generated in registers)
+  const double2* t1;
+  const double2* t2;
+};
+
 __device__ __forceinline__ double2 twg(const double2* __restrict__ tw, int e, bool inv) {
   double2 w = __ldg(tw + e);
   if (inv) w.y = -w.y;
@@ -167,14 +178,14 @@ __device__ __forceinline__ int t1_pos(int t, int i) {
 // v[n1] = x[t + T n1] in; out per t1_pos.  xb: this transform's exchange buffer
 // (WF<N>::XBUF doubles); tw: global W_N^k table.
 template <int N, bool INV>
-__device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const double2* __restrict__ tw) {
+__device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WTab tw) {
   if constexpr (N == 8) {
     dft8<INV>(v);
   } else {
     constexpr int T = WF<N>::T, S = WF<N>::S;
     dft16<INV>(v);
     if constexpr (T > 1) {
-      apply_powers<16>(v, twg(tw, t, INV));
+      apply_powers<16>(v, twg(tw.t0, t, INV));  // W_N^{t k1}
       if constexpr (T <= 16) {
         constexpr int C = 16 / T;
         PSWE_XPOSE(
@@ -213,7 +224,7 @@ __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const dou
 // ---- type 2 -------------------------------------------------------------------
 // input in t1_pos layout; out v[k2] = X[t + T k2].
 template <int N, bool INV>
-__device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const double2* __restrict__ tw) {
+__device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WTab tw) {
   if constexpr (N == 8) {
     dft8<INV>(v);
   } else {
@@ -223,8 +234,8 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const dou
         constexpr int C = 16 / T;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          dftL<T, INV>(v + c * T);                              // Z[n1][k1''], k1'' = 0..T-1
-          apply_powers<T>(v + c * T, twg(tw, t + T * c, INV));  // W_N^{n1 k1''}
+          dftL<T, INV>(v + c * T);                                 // Z[n1][k1''], k1'' = 0..T-1
+          apply_powers<T>(v + c * T, twg(tw.t0, t + T * c, INV));  // W_N^{n1 k1''}
         }
         PSWE_XPOSE(
             for (int c = 0; c < C; ++c) _Pragma("unroll") for (int k = 0; k < T; ++k) xb[(t + T * c) * S + k] = v[c * T + k].x,
@@ -250,11 +261,11 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const dou
         dft16<INV>(q);  // Z[n1][2 q' + h]
         // twiddle W_N^{n1 (2q'+h)} = W^{n1 h} (W^{2 n1})^{q'}
         if (h) {
-          const double2 b1 = twg(tw, n1, INV);
+          const double2 b1 = twg(tw.t0, n1, INV);
 #pragma unroll
           for (int k = 0; k < 16; ++k) q[k] = cmul(q[k], b1);
         }
-        apply_powers<16>(q, twg(tw, (2 * n1) & (N - 1), INV));
+        apply_powers<16>(q, twg(tw.t0, (2 * n1) & (N - 1), INV));
         PSWE_XPOSE(
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].x,
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].y,
@@ -263,6 +274,27 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const dou
       }
     }
     dft16<INV>(v);
+  }
+}
+
+// host/init helper: fill the WTab tables for length N (one thread per entry)
+__global__ void wtab_init_kernel(int N, double2* t1, double2* t2) {
+  const int T = N >= 16 ? N / 16 : 1;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 16 * T; idx += gridDim.x * blockDim.x) {
+    const int i = idx / T, t = idx % T;
+    long long e1 = (long long)t * i;  // W_N^{t k1}
+    long long e2;
+    if (T == 32) {
+      e2 = (long long)(t >> 1) * (2 * i + (t & 1));  // W_N^{n1 (2 q' + h)}
+    } else {
+      const int c = i / T, k = i % T;
+      e2 = (long long)(t + T * c) * k;  // W_N^{n1 k1''}
+    }
+    double s, c2;
+    sincospi(2.0 * (double)(e1 % N) / N, &s, &c2);
+    t1[idx] = make_double2(c2, -s);
+    sincospi(2.0 * (double)(e2 % N) / N, &s, &c2);
+    t2[idx] = make_double2(c2, -s);
   }
 }
 
