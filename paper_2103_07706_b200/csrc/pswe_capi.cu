@@ -84,6 +84,7 @@ struct pswe_ctx {
   bool quad_set = false;
   DevBuf<double> s_dev, w_dev;
   DevBuf<double> zero_s, one_w;  // single node s=0, w=1 for apply_nonlinear
+  std::vector<double> zero_live{0.0};
   // propagator
   int kind = 0, n_poly = 1;
   double Lambda = 0;
@@ -92,6 +93,11 @@ struct pswe_ctx {
   size_t chunk_bytes = size_t(160) << 20;
   DevBuf<double2> inter, slots, Uc, Ac, Ac2;
   double2* inter2 = nullptr;  // I2 region inside `inter`, after the CP phases of I1
+  // phase tables (c1, c2)[p][j][r] of the exact route: one for the quadrature,
+  // one for the single s = 0 node of apply_nonlinear; rebuilt when stale
+  DevBuf<double2> ctab_q, ctab_0;
+  bool ctab_q_valid = false, ctab_0_valid = false;
+  const double2* ctab_cur = nullptr;
   DevBuf<double2> full_tmp;  // stepper: edt, u1, u2 (3 states) + run ping-pong (2 states)
   DevBuf<int> flags;
   int* flags_host = nullptr;
@@ -162,9 +168,10 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
   const size_t smem = W::bytes(c->Kx);
   auto kern = passA_kernel<NX>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int blocks = (np * c->Ky + W::GPW - 1) / W::GPW;
+  const int nblk = np * ((c->Ky + W::GPW - 1) / W::GPW);
+  const int blocks = std::min(nblk, 4 * 148);
   ProfScope ps(c, 0, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->inter.p);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, c->inter.p);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -201,7 +208,8 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   const int cols = (c->Ky + W::GPW - 1) / W::GPW;
   const int blocks = cols * Gc;
   ProfScope ps(c, 2, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, c->inter2, c->slots.p, first);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, c->inter2, c->ctab_cur,
+                                            c->slots.p, first);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -260,6 +268,21 @@ int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first
 // then the ordered slot reduction.  `P` live phases in (s, w) device arrays.
 int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const double2* Uc, double2* Ac,
                 cudaStream_t st) {
+  // exact route: phase table (built once per quadrature / grid)
+  c->ctab_cur = nullptr;
+  if (c->kind == 0) {
+    const bool q = (s == c->s_dev.p);
+    DevBuf<double2>& tb = q ? c->ctab_q : c->ctab_0;
+    bool& valid = q ? c->ctab_q_valid : c->ctab_0_valid;
+    if (!valid) {
+      TRY(tb.alloc((size_t)P * c->Ky * c->Kx));
+      phase_table_kernel<<<elem_grid((size_t)P * c->Ky * c->Kx), 256, 0, st>>>(c->grid(), s, P, tb.p);
+      c->launches++;
+      CU(cudaGetLastError());
+      valid = true;
+    }
+    c->ctab_cur = tb.p;
+  }
   const size_t per_phase = (size_t)9 * c->Ky * c->nx;  // I1 (5 fields) + I2 (4 fields), double2
   int CP = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
   CP = std::min(CP, P);
@@ -267,7 +290,21 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   TRY(c->inter.alloc(per_phase * CP));
   c->inter2 = c->inter.p + (size_t)5 * c->Ky * c->nx * CP;
   TRY(c->slots.alloc((size_t)Gc * c->compact_elems()));
-  PhaseDev ph{s, w, P};
+  PhaseDev ph{s, w, P, 0.0, 0};
+  {
+    const std::vector<double>& sv = (s == c->s_dev.p) ? c->s_live : c->zero_live;
+    if (sv.size() >= 2) {
+      const double ds = (sv.back() - sv.front()) / (double)(sv.size() - 1);
+      bool uni = ds != 0.0;
+      for (size_t i = 1; i < sv.size() && uni; ++i)
+        uni = std::fabs((sv[i] - sv[i - 1]) - ds) <= 1e-12 * std::fabs(ds);
+      ph.ds = ds;
+      ph.uniform = uni ? 1 : 0;
+    } else {
+      ph.ds = 0.0;
+      ph.uniform = 1;  // a single phase: the rotor is only anchored, never advanced
+    }
+  }
   for (int p0 = 0; p0 < P; p0 += CP) {
     const int np = std::min(CP, P - p0);
     TRY(dispatchA(c, ph, p0, np, Uc, st));
@@ -507,6 +544,7 @@ int pswe_set_quadrature(pswe_ctx* c, int n_nodes, const double* s, const double*
   const size_t P = c->s_live.size();
   TRY(c->s_dev.alloc(P));
   TRY(c->w_dev.alloc(P));
+  c->ctab_q_valid = false;
   CU(cudaMemcpy(c->s_dev.p, c->s_live.data(), P * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(c->w_dev.p, c->w_live.data(), P * sizeof(double), cudaMemcpyHostToDevice));
   c->quad_set = true;

@@ -44,6 +44,8 @@ struct PhaseDev {
   const double* s;  // [P] live node shifts, ascending k
   const double* w;  // [P] weights
   int P;
+  double ds;        // uniform spacing of s (valid when uniform != 0)
+  int uniform;      // 1: s_p = s_0 + p ds to round-off -> phase rotors usable
 };
 
 // compact kx index of FFT position k (0..nx-1), or -1 outside the band
@@ -72,61 +74,95 @@ template <int NX>
 struct PassAW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 5;
+  // mbarrier | buffer [5][GPW][Kx] (u, v, eta, b, (c1,c2) -> u', v', depth in place) | xbuf per group
   static size_t bytes(int Kx) {
-    return (size_t)GPW * 3 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
+    return 16 + (size_t)GPW * 5 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
   }
 };
 
+// Persistent CTAs over "task blocks" (GPW consecutive ky columns of one
+// phase).  Per block: the compact U columns, b and the phase table's
+// (c1, c2) are TMA-bulk-prefetched (one buffer, refilled as soon as the FFT
+// inputs are in registers), the whole CTA applies e^{sL} per mode in place,
+// then warp f runs the inverse x-FFT of output field f (u, v, eta-b, ikx u,
+// ikx v) for the block's GPW columns and stores it to I1.
 template <int NX>
 __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
     passA_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, const double2* __restrict__ Uc,
-                 double2* __restrict__ I) {
+                 const double2* __restrict__ ctab, double2* __restrict__ I) {
   using W = PassAW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW;
-  extern __shared__ double2 dsm[];
+  extern __shared__ __align__(16) unsigned char sbytes[];
   const int Kx = G.Kx, Ky = G.Ky;
-  double2* stash = dsm;  // [GPW][3][Kx], already scaled by 1/(nx ny)
-  double* xbuf = reinterpret_cast<double*>(dsm + (size_t)GPW * 3 * Kx);
-  const int ntask = np * Ky;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
+  double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [5][GPW][Kx]
+  double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * 5 * Kx);
+  const bool tab = ctab != nullptr;
+  const int cols = (Ky + GPW - 1) / GPW;
+  const int nblk = np * cols;
+  const size_t KyKx = (size_t)Ky * Kx, fs = (size_t)GPW * Kx;
 
-  // e^{s L} once per (task, mode)
-  for (int idx = threadIdx.x; idx < GPW * Kx; idx += blockDim.x) {
-    const int tl = idx / Kx, r = idx % Kx;
-    const int task = blockIdx.x * GPW + tl;
-    C3 q = c3zero();
-    if (task < ntask) {
-      const int pl = task / Ky, j = task % Ky;
-      q = {Uc[cidx(G, 0, j, r)], Uc[cidx(G, 1, j, r)], Uc[cidx(G, 2, j, r)]};
-      q = expL(ph.s[p0 + pl], q, G.ph, G.kxc[r], G.kyc[j], pr);
-      q.e = csub(q.e, G.bc[(size_t)j * Kx + r]);
-    }
-    double2* st = stash + (size_t)tl * 3 * Kx;
-    st[r] = cscale(G.inv_n2, q.u);
-    st[Kx + r] = cscale(G.inv_n2, q.v);
-    st[2 * Kx + r] = cscale(G.inv_n2, q.e);
+  // block -> (phase pl, first column j0, ncol columns): contiguous in U, b, ctab
+  auto prefetch = [&](int blk) {
+    const int pl = blk / cols, j0 = (blk % cols) * GPW;
+    const int ncol = min(GPW, Ky - j0);
+    const uint32_t seg = (uint32_t)(ncol * Kx * sizeof(double2));
+    mbar_arrive_expect_tx(bar, (tab ? 5 : 4) * seg);
+    for (int f = 0; f < 3; ++f) bulk_g2s(buf + f * fs, Uc + f * KyKx + (size_t)j0 * Kx, seg, bar);
+    bulk_g2s(buf + 3 * fs, G.bc + (size_t)j0 * Kx, seg, bar);
+    if (tab) bulk_g2s(buf + 4 * fs, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, seg, bar);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    if ((int)blockIdx.x < nblk) prefetch(blockIdx.x);
   }
   __syncthreads();
 
-  const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;  // warp = field
+  const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;  // warp = output field
   const int tl = lane / T, t = lane % T;
-  const int task = blockIdx.x * GPW + tl;
-  const bool active = task < ntask;
-  const int pl = active ? task / Ky : 0, j = active ? task % Ky : 0;
-  const double2* st = stash + (size_t)tl * 3 * Kx + (f < 3 ? f : f - 3) * Kx;
-  double2 v[P];
-#pragma unroll
-  for (int n1 = 0; n1 < P; ++n1) {
-    const int r = band_r(t + T * n1, NX, G.kxm, Kx);
-    v[n1] = czero();
-    if (r >= 0) {
-      v[n1] = st[r];
-      if (f >= 3) v[n1] = cik(G.kxc[r], v[n1]);
+  double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
+  const int src = f < 3 ? f : f - 3;
+  int it = 0;
+#pragma unroll 1
+  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+    const int pl = blk / cols, j0 = (blk % cols) * GPW;
+    const int ncol = min(GPW, Ky - j0);
+    const double s = ph.s[p0 + pl];
+    mbar_wait(bar, it & 1);
+    // e^{sL} per mode in place: (u, v, eta, b) -> (u', v', eta' - b) / (nx ny)
+    for (int idx = threadIdx.x; idx < ncol * Kx; idx += blockDim.x) {
+      const int tt = idx / Kx, r = idx % Kx;
+      double2* e = buf + idx;
+      C3 q = {e[0], e[fs], e[2 * fs]};
+      if (tab)
+        q = exp_c12(e[4 * fs], q, G.ph, G.kxc[r], G.kyc[j0 + tt]);
+      else
+        q = expL(s, q, G.ph, G.kxc[r], G.kyc[j0 + tt], pr);
+      e[0] = cscale(G.inv_n2, q.u);
+      e[fs] = cscale(G.inv_n2, q.v);
+      e[2 * fs] = cscale(G.inv_n2, csub(q.e, e[3 * fs]));
     }
-  }
-  wfft_t1<NX, true>(v, t, xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF, G.twx);
-  if (active) {
+    __syncthreads();
+    const bool active = tl < ncol;
+    const double2* st = buf + (size_t)src * fs + (size_t)tl * Kx;
+    double2 v[P];
 #pragma unroll
-    for (int i = 0; i < P; ++i) I[iidx(G, pl, t1_pos<NX>(t, i), f, j)] = v[i];
+    for (int n1 = 0; n1 < P; ++n1) {
+      const int r = band_r(t + T * n1, NX, NX / 3, 2 * (NX / 3) + 1);
+      v[n1] = czero();
+      if (active && r >= 0) {
+        v[n1] = st[r];
+        if (f >= 3) v[n1] = cik(G.kxc[r], v[n1]);
+      }
+    }
+    __syncthreads();  // buffer consumed: refill it for the next block while the FFTs run
+    if (threadIdx.x == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
+    wfft_t1<NX, true>(v, t, xb, G.twx);
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) I[iidx(G, pl, t1_pos<NX>(t, i), f, j0 + tl)] = v[i];
+    }
   }
 }
 
@@ -371,7 +407,7 @@ struct PassCW {
 template <int NX>
 __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
     passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
-                 double2* __restrict__ slots, int first_chunk) {
+                 const double2* __restrict__ ctab, double2* __restrict__ slots, int first_chunk) {
   using W = PassCW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, CPT = W::CPT;
   extern __shared__ __align__(16) unsigned char sbytes[];
@@ -434,7 +470,13 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
         const double kx = G.kxc[r], ky = G.kyc[j0 + tt];
         const double2 gx = cik(kx, Ft[2 * Kx + r]), gy = cik(ky, Ft[3 * Kx + r]);
         C3 q = {Ft[r], Ft[Kx + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
-        q = expL(-s, q, G.ph, kx, ky, pr);
+        if (ctab) {
+          double2 c12 = ctab[(size_t)(p0 + pl) * KyKx + (size_t)(j0 + tt) * Kx + r];
+          c12.x = -c12.x;  // e^{-sL}: c1(-s) = -c1(s), c2(-s) = c2(s)
+          q = exp_c12(c12, q, G.ph, kx, ky);
+        } else {
+          q = expL(-s, q, G.ph, kx, ky, pr);
+        }
         acc[c] = c3add(acc[c], c3scale(w, q));
       }
     }
@@ -623,6 +665,31 @@ __global__ void stage3_kernel(GridDev G, Prop pr, double dt, Full3 edt, Full3 u2
       st3(out, i, o);
     }
     flag_nonfinite(o, 3, flags);
+  }
+}
+
+// phase table (c1, c2)[p][j][r] of the exact exponential for every live phase
+// and compact mode, evaluated with the reference's formula
+// (propagator.py:100-103): c1 = sin(w s)/w, c2 = (1 - cos w s)/w^2.
+__global__ void phase_table_kernel(GridDev G, const double* __restrict__ s, int P, double2* __restrict__ tab) {
+  const size_t KyKx = (size_t)G.Ky * G.Kx, n = (size_t)P * KyKx;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int p = (int)(i / KyKx);
+    const int rem = (int)(i % KyKx);
+    const int j = rem / G.Kx, r = rem % G.Kx;
+    const double om = omega_of(G.ph, G.kxc[r], G.kyc[j]);
+    const double t = s[p];
+    double c1, c2;
+    if (om > 0.0) {
+      double sn, cs;
+      sincos(om * t, &sn, &cs);
+      c1 = sn / om;
+      c2 = (1.0 - cs) / (om * om);
+    } else {
+      c1 = t;
+      c2 = 0.5 * t * t;
+    }
+    tab[i] = cmk(c1, c2);
   }
 }
 
