@@ -74,9 +74,10 @@ template <int NX>
 struct PassAW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 5;
-  // mbarrier | buffer [5][GPW][Kx] (u, v, eta, b, (c1,c2) -> u', v', depth in place) | xbuf per group
+  // mbarrier | buffer [5][GPW][Kx] (u, v, eta, b, (c1,c2) -> u', v', depth in place) | xbuf per group | kx [Kx]
   static size_t bytes(int Kx) {
-    return 16 + (size_t)GPW * 5 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
+    return 16 + (size_t)GPW * 5 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) +
+           (size_t)Kx * sizeof(double);
   }
 };
 
@@ -93,36 +94,42 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
   using W = PassAW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW;
   extern __shared__ __align__(16) unsigned char sbytes[];
-  const int Kx = G.Kx, Ky = G.Ky;
+  constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
+  const int Ky = G.Ky;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
   double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [5][GPW][Kx]
   double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * 5 * Kx);
+  double* kxs = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;
   const bool tab = ctab != nullptr;
   const int cols = (Ky + GPW - 1) / GPW;
   const int nblk = np * cols;
   const size_t KyKx = (size_t)Ky * Kx, fs = (size_t)GPW * Kx;
+  const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;  // warp = output field
+  for (int i = threadIdx.x; i < Kx; i += blockDim.x) kxs[i] = G.kxc[i];
 
-  // block -> (phase pl, first column j0, ncol columns): contiguous in U, b, ctab
+  // block -> (phase pl, first column j0, ncol columns): contiguous in U, b, ctab.
+  // Warp 0: lane 0 posts the byte count, lanes 0..4 each issue one bulk copy.
   auto prefetch = [&](int blk) {
     const int pl = blk / cols, j0 = (blk % cols) * GPW;
     const int ncol = min(GPW, Ky - j0);
     const uint32_t seg = (uint32_t)(ncol * Kx * sizeof(double2));
-    mbar_arrive_expect_tx(bar, (tab ? 5 : 4) * seg);
-    for (int f = 0; f < 3; ++f) bulk_g2s(buf + f * fs, Uc + f * KyKx + (size_t)j0 * Kx, seg, bar);
-    bulk_g2s(buf + 3 * fs, G.bc + (size_t)j0 * Kx, seg, bar);
-    if (tab) bulk_g2s(buf + 4 * fs, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, seg, bar);
+    if (lane == 0) mbar_arrive_expect_tx(bar, (tab ? 5 : 4) * seg);
+    __syncwarp();
+    if (lane < 3) bulk_g2s(buf + lane * fs, Uc + lane * KyKx + (size_t)j0 * Kx, seg, bar);
+    if (lane == 3) bulk_g2s(buf + 3 * fs, G.bc + (size_t)j0 * Kx, seg, bar);
+    if (lane == 4 && tab) bulk_g2s(buf + 4 * fs, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, seg, bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    if ((int)blockIdx.x < nblk) prefetch(blockIdx.x);
   }
   __syncthreads();
+  if (f == 0 && (int)blockIdx.x < nblk) prefetch(blockIdx.x);
 
-  const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;  // warp = output field
   const int tl = lane / T, t = lane % T;
   double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
   const int src = f < 3 ? f : f - 3;
+  const size_t ostride = (size_t)5 * Ky;  // I1 row stride (one physical x)
   int it = 0;
 #pragma unroll 1
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
@@ -136,9 +143,9 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
       double2* e = buf + idx;
       C3 q = {e[0], e[fs], e[2 * fs]};
       if (tab)
-        q = exp_c12(e[4 * fs], q, G.ph, G.kxc[r], G.kyc[j0 + tt]);
+        q = exp_c12(e[4 * fs], q, G.ph, kxs[r], G.kyc[j0 + tt]);
       else
-        q = expL(s, q, G.ph, G.kxc[r], G.kyc[j0 + tt], pr);
+        q = expL(s, q, G.ph, kxs[r], G.kyc[j0 + tt], pr);
       e[0] = cscale(G.inv_n2, q.u);
       e[fs] = cscale(G.inv_n2, q.v);
       e[2 * fs] = cscale(G.inv_n2, csub(q.e, e[3 * fs]));
@@ -149,19 +156,20 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
     double2 v[P];
 #pragma unroll
     for (int n1 = 0; n1 < P; ++n1) {
-      const int r = band_r(t + T * n1, NX, NX / 3, 2 * (NX / 3) + 1);
+      const int r = band_r(t + T * n1, NX, NX / 3, Kx);
       v[n1] = czero();
       if (active && r >= 0) {
         v[n1] = st[r];
-        if (f >= 3) v[n1] = cik(G.kxc[r], v[n1]);
+        if (f >= 3) v[n1] = cik(kxs[r], v[n1]);
       }
     }
     __syncthreads();  // buffer consumed: refill it for the next block while the FFTs run
-    if (threadIdx.x == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
+    if (f == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
     wfft_t1<NX, true>(v, t, xb, G.twx);
     if (active) {
+      double2* ob = I + ((size_t)pl * NX * 5 + f) * Ky + j0 + tl;
 #pragma unroll
-      for (int i = 0; i < P; ++i) I[iidx(G, pl, t1_pos<NX>(t, i), f, j0 + tl)] = v[i];
+      for (int i = 0; i < P; ++i) ob[(size_t)t1_pos<NX>(t, i) * ostride] = v[i];
     }
   }
 }
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   using W = PassBW<NY>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW;
   extern __shared__ __align__(16) unsigned char sbytes[];
-  const int Ky = Gd.Ky;
+  constexpr int Ky = NY / 3 + 1;  // == Gd.Ky
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane % T, g = lane / T;
   unsigned char* wbase = sbytes + (size_t)warp * ((W::warp_bytes(Ky) + 15) / 16 * 16);
@@ -390,20 +398,19 @@ struct PassCW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 4;
   static constexpr int CPT = 3;  // combine modes per thread (GPW * Kx <= 3 * 128)
-  // 2 mbarriers | prefetch [4][GPW][NX] | F [GPW][4][Kx] | xbuf per group
+  // mbarrier | prefetch [4][GPW][NX] | (c1,c2) [GPW][Kx] | F [GPW][4][Kx] | xbuf per group | kx [Kx]
   static size_t bytes(int Kx) {
-    return 16 + (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * 4 * Kx * sizeof(double2) +
-           (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
+    return 16 + (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * 5 * Kx * sizeof(double2) +
+           (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) + (size_t)Kx * sizeof(double);
   }
 };
 
 // CTA = (GPW ky columns) x (phase group g of the chunk).  Loops over the
 // group's phases in ascending order; each phase's 4 product columns
-// (contiguous in I2) are TMA-bulk-prefetched while the previous phase
-// computes.  Warp f transforms field f; then every thread combines its modes
-// (flux divergence, e^{-sL}, weight) into register accumulators, which are
-// added to the group's slot once at the end (slot values from earlier chunks
-// are read after the loop).
+// (contiguous in I2) and its phase-table columns are TMA-bulk-prefetched
+// while the previous phase computes.  Warp f transforms field f; then every
+// thread combines its modes (flux divergence, e^{-sL}, weight) into register
+// accumulators, which are added to the group's slot once at the end.
 template <int NX>
 __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
     passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
@@ -411,33 +418,41 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   using W = PassCW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, CPT = W::CPT;
   extern __shared__ __align__(16) unsigned char sbytes[];
-  const int Kx = G.Kx, Ky = G.Ky;
+  constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
+  const int Ky = G.Ky;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
   double2* pre = reinterpret_cast<double2*>(sbytes + 16);  // [4][GPW][NX]
-  double2* F = pre + (size_t)4 * GPW * NX;                  // [GPW][4][Kx]
+  double2* ctb = pre + (size_t)4 * GPW * NX;                // [GPW][Kx]
+  double2* F = ctb + (size_t)GPW * Kx;                      // [GPW][4][Kx]
   double* xbuf = reinterpret_cast<double*>(F + (size_t)GPW * 4 * Kx);
+  double* kxs = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;
   const int cols = (Ky + GPW - 1) / GPW;
   const int cb = blockIdx.x % cols, g = blockIdx.x / cols;
   const int lo = (int)(((long long)g * np) / Gc), hi = (int)(((long long)(g + 1) * np) / Gc);
   const size_t KyKx = (size_t)Ky * Kx, KyNX = (size_t)Ky * NX;
   const int j0 = cb * GPW;
   const int ncol = min(GPW, Ky - j0);  // active columns of this CTA (contiguous in I2)
+  const bool tab = ctab != nullptr;
+  const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < Kx; i += blockDim.x) kxs[i] = G.kxc[i];
 
+  // warp 0: lane 0 posts the byte count, lanes 0..4 each issue one bulk copy
   auto prefetch = [&](int pl) {
-    // fields f: the CTA's ncol columns are contiguous: I2[pl][f][j0 .. j0+ncol)[x]
     const uint32_t seg = (uint32_t)(ncol * NX * sizeof(double2));
-    mbar_arrive_expect_tx(bar, 4 * seg);
-    for (int f = 0; f < 4; ++f)
-      bulk_g2s(pre + (size_t)f * GPW * NX, I2 + ((size_t)pl * 4 + f) * KyNX + (size_t)j0 * NX, seg, bar);
+    const uint32_t tseg = (uint32_t)(ncol * Kx * sizeof(double2));
+    if (lane == 0) mbar_arrive_expect_tx(bar, 4 * seg + (tab ? tseg : 0));
+    __syncwarp();
+    if (lane < 4)
+      bulk_g2s(pre + (size_t)lane * GPW * NX, I2 + ((size_t)pl * 4 + lane) * KyNX + (size_t)j0 * NX, seg, bar);
+    if (lane == 4 && tab) bulk_g2s(ctb, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg, bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    if (lo < hi) prefetch(lo);
   }
   __syncthreads();
+  if (f == 0 && lo < hi) prefetch(lo);
 
-  const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;
   const int tl = lane / T, t = lane % T;
   double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
   double2* Ff = F + ((size_t)tl * 4 + f) * Kx;
@@ -451,12 +466,11 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
     double2 v[P];
 #pragma unroll
     for (int n1 = 0; n1 < P; ++n1) v[n1] = mine[t + T * n1];
-    __syncthreads();  // prefetch buffer consumed; F free (previous combine done)
-    if (threadIdx.x == 0 && pl + 1 < hi) prefetch(pl + 1);
+    // the combine below reads ctb, so the refill waits for the end of this phase
     wfft_t1<NX, false>(v, t, xb, G.twx);
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-      const int r = band_r(t1_pos<NX>(t, i), NX, G.kxm, Kx);
+      const int r = band_r(t1_pos<NX>(t, i), NX, NX / 3, Kx);
       if (r >= 0) Ff[r] = v[i];
     }
     __syncthreads();
@@ -467,11 +481,11 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
       const int tt = idx / Kx, r = idx % Kx;
       if (tt < ncol) {
         const double2* Ft = F + (size_t)tt * 4 * Kx;
-        const double kx = G.kxc[r], ky = G.kyc[j0 + tt];
+        const double kx = kxs[r], ky = G.kyc[j0 + tt];
         const double2 gx = cik(kx, Ft[2 * Kx + r]), gy = cik(ky, Ft[3 * Kx + r]);
         C3 q = {Ft[r], Ft[Kx + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
-        if (ctab) {
-          double2 c12 = ctab[(size_t)(p0 + pl) * KyKx + (size_t)(j0 + tt) * Kx + r];
+        if (tab) {
+          double2 c12 = ctb[idx];
           c12.x = -c12.x;  // e^{-sL}: c1(-s) = -c1(s), c2(-s) = c2(s)
           q = exp_c12(c12, q, G.ph, kx, ky);
         } else {
@@ -480,6 +494,8 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
         acc[c] = c3add(acc[c], c3scale(w, q));
       }
     }
+    __syncthreads();  // pre, ctb and F consumed
+    if (f == 0 && pl + 1 < hi) prefetch(pl + 1);
   }
   // slot (+)= this group's phases, in chunk order
   double2* slot = slots + (size_t)g * 3 * KyKx;
