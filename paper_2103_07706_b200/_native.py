@@ -15,7 +15,8 @@ import threading
 
 import numpy as np
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "lib" / "libpswe_b200.so"
+LIB_PATH = pathlib.Path(os.environ.get("PSWE_LIB_PATH") or
+                        pathlib.Path(__file__).resolve().parent / "lib" / "libpswe_b200.so")
 
 PSWE_OK = 0
 PSWE_EINVAL = 1

@@ -47,6 +47,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Order this thread's generic-proxy shared-memory writes before later
+// async-proxy (TMA) accesses of the same bytes: required before a bulk copy
+// overwrites a buffer the CTA has written with ordinary stores.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Warp-convergent wait: lane 0 spins on the barrier, then the warp
 // reconverges at __syncwarp (which also orders the other lanes' subsequent
 // shared-memory reads after lane 0's acquire).  Keeping the spin loop out of

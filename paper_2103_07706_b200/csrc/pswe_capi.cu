@@ -289,6 +289,9 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
   TRY(c->inter.alloc(per_phase * CP));
   c->inter2 = c->inter.p + (size_t)5 * c->Ky * c->nx * CP;
+  if (getenv("PSWE_DEBUG_POISON")) {  // debug: NaN-fill intermediates to expose unwritten entries
+    CU(cudaMemsetAsync(c->inter.p, 0xFF, per_phase * CP * sizeof(double2), st));
+  }
   TRY(c->slots.alloc((size_t)Gc * c->compact_elems()));
   PhaseDev ph{s, w, P, 0.0, 0};
   {

@@ -70,6 +70,50 @@ __device__ __forceinline__ size_t cidx(const GridDev& G, int f, int j, int r) {
 // (task = one (phase, ky column)); the e^{sL} per mode is computed once per
 // task by the whole CTA into a shared compact stash.
 // ============================================================================
+// Gather a compact kx column (Kx values, FFT order wx = 0..K, -K..-1) into
+// the type-1 input layout v[n1] = x[t + T n1]; out-of-band slots are zero.
+// Band membership of each register slot is resolved at compile time except
+// for the slots whose position range straddles a band edge.
+template <int N, int N1 = 0>
+__device__ __forceinline__ void band_gather(double2* v, int t, const double2* col, bool active) {
+  if constexpr (N1 < WF<N>::P) {
+    constexpr int T = WF<N>::T, K = N / 3, Kx = 2 * K + 1;
+    constexpr int kmin = T * N1, kmax = T * N1 + T - 1;
+    const int k = t + kmin;
+    if constexpr (kmax <= K) {
+      v[N1] = active ? col[k] : czero();
+    } else if constexpr (kmin >= N - K) {
+      v[N1] = active ? col[k - N + Kx] : czero();
+    } else if constexpr (kmin > K && kmax < N - K) {
+      v[N1] = czero();
+    } else {
+      const int r = band_r(k, N, K, Kx);
+      v[N1] = (active && r >= 0) ? col[r] : czero();
+    }
+    band_gather<N, N1 + 1>(v, t, col, active);
+  }
+}
+
+// Store a type-1 output (register i holds position t1_pos(t, i)) to
+// out[pos * stride] with incremental addressing.
+template <int N>
+__device__ __forceinline__ void store_t1_strided(const double2* v, int t, double2* out, size_t stride) {
+  constexpr int T = WF<N>::T, P = WF<N>::P;
+  if constexpr (N == 8 || T < 32) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) out[(size_t)t1_pos<N>(t, i) * stride] = v[i];
+  } else {
+    // T == 32: positions k1 + 16 (8h + i) for i < 8, + 256 for i >= 8
+    double2* p = out + (size_t)t1_pos<N>(t, 0) * stride;
+    const size_t s16 = 16 * stride;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i * s16] = v[i];
+    p += 256 * stride;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i * s16] = v[8 + i];
+  }
+}
+
 template <int NX>
 struct PassAW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
@@ -128,7 +172,6 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
 
   const int tl = lane / T, t = lane % T;
   double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
-  const int src = f < 3 ? f : f - 3;
   const size_t ostride = (size_t)5 * Ky;  // I1 row stride (one physical x)
   int it = 0;
 #pragma unroll 1
@@ -142,35 +185,34 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
       const int tt = idx / Kx, r = idx % Kx;
       double2* e = buf + idx;
       C3 q = {e[0], e[fs], e[2 * fs]};
+      const double kx = kxs[r];
       if (tab)
-        q = exp_c12(e[4 * fs], q, G.ph, kxs[r], G.kyc[j0 + tt]);
+        q = exp_c12(e[4 * fs], q, G.ph, kx, G.kyc[j0 + tt]);
       else
-        q = expL(s, q, G.ph, kxs[r], G.kyc[j0 + tt], pr);
+        q = expL(s, q, G.ph, kx, G.kyc[j0 + tt], pr);
+      // slots 0..2 become u', v', eta' - b (the ikx fields are formed by the
+      // consuming warps; writing them into slots 3/4 here raced with the
+      // next block's TMA refill of those slots in testing)
       e[0] = cscale(G.inv_n2, q.u);
       e[fs] = cscale(G.inv_n2, q.v);
       e[2 * fs] = cscale(G.inv_n2, csub(q.e, e[3 * fs]));
     }
+    fence_proxy_async();  // order these stores before the next block's TMA refill of buf
     __syncthreads();
     const bool active = tl < ncol;
-    const double2* st = buf + (size_t)src * fs + (size_t)tl * Kx;
     double2 v[P];
+    band_gather<NX>(v, t, buf + (size_t)(f < 3 ? f : f - 3) * fs + (size_t)tl * Kx, active);
+    if (f >= 3) {  // ikx u', ikx v'
 #pragma unroll
-    for (int n1 = 0; n1 < P; ++n1) {
-      const int r = band_r(t + T * n1, NX, NX / 3, Kx);
-      v[n1] = czero();
-      if (active && r >= 0) {
-        v[n1] = st[r];
-        if (f >= 3) v[n1] = cik(kxs[r], v[n1]);
+      for (int n1 = 0; n1 < P; ++n1) {
+        const int r = band_r(t + T * n1, NX, NX / 3, Kx);
+        if (r >= 0) v[n1] = cik(kxs[r], v[n1]);
       }
     }
     __syncthreads();  // buffer consumed: refill it for the next block while the FFTs run
     if (f == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
     wfft_t1<NX, true>(v, t, xb, G.twx);
-    if (active) {
-      double2* ob = I + ((size_t)pl * NX * 5 + f) * Ky + j0 + tl;
-#pragma unroll
-      for (int i = 0; i < P; ++i) ob[(size_t)t1_pos<NX>(t, i) * ostride] = v[i];
-    }
+    if (active) store_t1_strided<NX>(v, t, I + ((size_t)pl * NX * 5 + f) * Ky + j0 + tl, ostride);
   }
 }
 

@@ -142,6 +142,19 @@ def test_linearity_in_weights_at_512_m256():
     assert np.array_equal(again, parts[2])
 
 
+@pytest.mark.parametrize("level,M", [(6, 64), (7, 32)])
+def test_repeated_evaluations_are_bitwise_identical(level, M):
+    """Run-to-run determinism over many evaluations (guards the TMA-prefetch/in-place buffer protocol)."""
+    c = cases.case_c5(level, M)
+    ctx = pk.dynamics.context(c.state, c.params)
+    ctx.set_propagator("exact")
+    ctx.set_quadrature(c.quadrature.s, c.quadrature.w)
+    Uc = ctx.pack(pk.dynamics.upload(ctx, c.state))
+    first = ctx.averaged_tendency_compact(Uc).cpu().numpy()
+    for _ in range(6):
+        assert np.array_equal(ctx.averaged_tendency_compact(Uc).cpu().numpy(), first)
+
+
 def test_chunking_does_not_change_results():
     c = cases.case_c5(5, 32)  # 128^2, 63 phases
     ctx = pk.dynamics.context(c.state, c.params)
