@@ -90,9 +90,10 @@ struct pswe_ctx {
   double Lambda = 0;
   DevBuf<double> a_dev;
   // scratch
-  size_t chunk_bytes = size_t(160) << 20;
+  size_t chunk_bytes = size_t(96) << 20;
   DevBuf<double2> inter, slots, Uc, Ac, Ac2;
-  double2* inter2 = nullptr;  // I2 region inside `inter`, after the CP phases of I1
+  cudaStream_t st2 = nullptr;  // second chunk lane
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // phase tables (c1, c2)[p][j][r] of the exact route: one for the quadrature,
   // one for the single s = 0 node of apply_nonlinear; rebuilt when stale
   DevBuf<double2> ctab_q, ctab_0;
@@ -163,7 +164,7 @@ struct ProfScope {
 
 // ---------------------------------------------------------------- dispatch
 template <int NX>
-int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, cudaStream_t st) {
+int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, cudaStream_t st) {
   using W = PassAW<NX>;
   const size_t smem = W::bytes(c->Kx);
   auto kern = passA_kernel<NX>;
@@ -171,21 +172,21 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
   const int nblk = np * ((c->Ky + W::GPW - 1) / W::GPW);
   const int blocks = std::min(nblk, 4 * 148);
   ProfScope ps(c, 0, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, c->inter.p);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, I1);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
 
 template <int NY>
-int launchB(pswe_ctx* c, int np, cudaStream_t st) {
+int launchB(pswe_ctx* c, int np, const double2* I1, double2* I2, cudaStream_t st) {
   using W = PassBW<NY>;
   const size_t smem = W::bytes(c->Ky);
   auto kern = passB_kernel<NY>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, c->inter.p, c->inter2);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, I1, I2);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -195,12 +196,14 @@ template <int NX>
 int pass_c_groups(const pswe_ctx* c, int CP) {
   // enough CTAs for ~4 per SM, each looping over CP/Gc phases
   const int cols = (c->Ky + PassCW<NX>::GPW - 1) / PassCW<NX>::GPW;
-  const int want = (4 * 148 + cols - 1) / cols;
+  int want = (3 * 148 + cols - 1) / cols;
+  if (const char* e = getenv("PSWE_GC")) want = atoi(e);  // tuning experiments
   return std::max(1, std::min(want, CP));
 }
 
 template <int NX>
-int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, cudaStream_t st) {
+int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
+            double2* slots, cudaStream_t st) {
   using W = PassCW<NX>;
   const size_t smem = W::bytes(c->Kx);
   auto kern = passC_kernel<NX>;
@@ -208,34 +211,33 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   const int cols = (c->Ky + W::GPW - 1) / W::GPW;
   const int blocks = cols * Gc;
   ProfScope ps(c, 2, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, c->inter2, c->ctab_cur,
-                                            c->slots.p, first);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, I2, c->ctab_cur, slots, first);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
 
-int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, cudaStream_t st) {
+int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, cudaStream_t st) {
   switch (c->nx) {
-    case 8: return launchA<8>(c, ph, p0, np, Uc, st);
-    case 16: return launchA<16>(c, ph, p0, np, Uc, st);
-    case 32: return launchA<32>(c, ph, p0, np, Uc, st);
-    case 64: return launchA<64>(c, ph, p0, np, Uc, st);
-    case 128: return launchA<128>(c, ph, p0, np, Uc, st);
-    case 256: return launchA<256>(c, ph, p0, np, Uc, st);
-    case 512: return launchA<512>(c, ph, p0, np, Uc, st);
+    case 8: return launchA<8>(c, ph, p0, np, Uc, I1, st);
+    case 16: return launchA<16>(c, ph, p0, np, Uc, I1, st);
+    case 32: return launchA<32>(c, ph, p0, np, Uc, I1, st);
+    case 64: return launchA<64>(c, ph, p0, np, Uc, I1, st);
+    case 128: return launchA<128>(c, ph, p0, np, Uc, I1, st);
+    case 256: return launchA<256>(c, ph, p0, np, Uc, I1, st);
+    case 512: return launchA<512>(c, ph, p0, np, Uc, I1, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
-int dispatchB(pswe_ctx* c, int np, cudaStream_t st) {
+int dispatchB(pswe_ctx* c, int np, const double2* I1, double2* I2, cudaStream_t st) {
   switch (c->ny) {
-    case 8: return launchB<8>(c, np, st);
-    case 16: return launchB<16>(c, np, st);
-    case 32: return launchB<32>(c, np, st);
-    case 64: return launchB<64>(c, np, st);
-    case 128: return launchB<128>(c, np, st);
-    case 256: return launchB<256>(c, np, st);
-    case 512: return launchB<512>(c, np, st);
+    case 8: return launchB<8>(c, np, I1, I2, st);
+    case 16: return launchB<16>(c, np, I1, I2, st);
+    case 32: return launchB<32>(c, np, I1, I2, st);
+    case 64: return launchB<64>(c, np, I1, I2, st);
+    case 128: return launchB<128>(c, np, I1, I2, st);
+    case 256: return launchB<256>(c, np, I1, I2, st);
+    case 512: return launchB<512>(c, np, I1, I2, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported ny = %d", c->ny);
 }
@@ -251,15 +253,16 @@ int groupsC(const pswe_ctx* c, int CP) {
   }
 }
 
-int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, cudaStream_t st) {
+int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
+              double2* slots, cudaStream_t st) {
   switch (c->nx) {
-    case 8: return launchC<8>(c, ph, p0, np, Gc, first, st);
-    case 16: return launchC<16>(c, ph, p0, np, Gc, first, st);
-    case 32: return launchC<32>(c, ph, p0, np, Gc, first, st);
-    case 64: return launchC<64>(c, ph, p0, np, Gc, first, st);
-    case 128: return launchC<128>(c, ph, p0, np, Gc, first, st);
-    case 256: return launchC<256>(c, ph, p0, np, Gc, first, st);
-    case 512: return launchC<512>(c, ph, p0, np, Gc, first, st);
+    case 8: return launchC<8>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 16: return launchC<16>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 32: return launchC<32>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 64: return launchC<64>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 128: return launchC<128>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 256: return launchC<256>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 512: return launchC<512>(c, ph, p0, np, Gc, first, I2, slots, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
@@ -287,12 +290,18 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   int CP = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
   CP = std::min(CP, P);
   const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
-  TRY(c->inter.alloc(per_phase * CP));
-  c->inter2 = c->inter.p + (size_t)5 * c->Ky * c->nx * CP;
+  // Two chunk "lanes" on two streams when there is more than one chunk: the
+  // next chunk's passes fill the previous chunk's launch tails.  Each lane
+  // has its own intermediates and slot set; chunks alternate lanes, every
+  // slot accumulates its lane's chunks in order and the final reduction sums
+  // lane 0's slots then lane 1's -- a fixed order, so results stay bitwise
+  // deterministic.
+  const int lanes = (P > CP) ? 2 : 1;
+  TRY(c->inter.alloc(per_phase * CP * lanes));
+  TRY(c->slots.alloc((size_t)lanes * Gc * c->compact_elems()));
   if (getenv("PSWE_DEBUG_POISON")) {  // debug: NaN-fill intermediates to expose unwritten entries
-    CU(cudaMemsetAsync(c->inter.p, 0xFF, per_phase * CP * sizeof(double2), st));
+    CU(cudaMemsetAsync(c->inter.p, 0xFF, per_phase * CP * lanes * sizeof(double2), st));
   }
-  TRY(c->slots.alloc((size_t)Gc * c->compact_elems()));
   PhaseDev ph{s, w, P, 0.0, 0};
   {
     const std::vector<double>& sv = (s == c->s_dev.p) ? c->s_live : c->zero_live;
@@ -308,15 +317,29 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
       ph.uniform = 1;  // a single phase: the rotor is only anchored, never advanced
     }
   }
-  for (int p0 = 0; p0 < P; p0 += CP) {
+  cudaStream_t lst[2] = {st, c->st2};
+  if (lanes == 2) {
+    CU(cudaEventRecord(c->ev_fork, st));
+    CU(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+  }
+  int chunk = 0;
+  for (int p0 = 0; p0 < P; p0 += CP, ++chunk) {
     const int np = std::min(CP, P - p0);
-    TRY(dispatchA(c, ph, p0, np, Uc, st));
-    TRY(dispatchB(c, np, st));
-    TRY(dispatchC(c, ph, p0, np, Gc, p0 == 0 ? 1 : 0, st));
+    const int L = chunk % lanes;
+    double2* I1 = c->inter.p + (size_t)L * per_phase * CP;
+    double2* I2 = I1 + (size_t)5 * c->Ky * c->nx * CP;
+    double2* sl = c->slots.p + (size_t)L * Gc * c->compact_elems();
+    TRY(dispatchA(c, ph, p0, np, Uc, I1, lst[L]));
+    TRY(dispatchB(c, np, I1, I2, lst[L]));
+    TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
+  }
+  if (lanes == 2) {
+    CU(cudaEventRecord(c->ev_join, c->st2));
+    CU(cudaStreamWaitEvent(st, c->ev_join, 0));
   }
   const size_t n = c->compact_elems();
   ProfScope ps(c, 3, st);
-  reduce_slots_kernel<<<elem_grid(n), 256, 0, st>>>(c->slots.p, Gc, n, Ac);
+  reduce_slots_kernel<<<elem_grid(n), 256, 0, st>>>(c->slots.p, lanes * Gc, n, Ac);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -487,6 +510,12 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
       return rc;
     }
   }
+  if (cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    pswe_destroy(c);
+    return set_err(PSWE_ECUDA, "stream/event creation failed");
+  }
   if (cudaMallocHost(&c->flags_host, sizeof(int)) != cudaSuccess) {
     pswe_destroy(c);
     return set_err(PSWE_ECUDA, "cudaMallocHost failed");
@@ -510,6 +539,9 @@ void pswe_destroy(pswe_ctx* c) {
   c->flags.release();
   if (c->flags_host) cudaFreeHost(c->flags_host);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->st2) cudaStreamDestroy(c->st2);
   delete c;
 }
 
