@@ -339,6 +339,9 @@ def run_ours(args, ws, rank, local):
     sweep = None
     if not args.no_sweep and rank == 0:
         sweep = run_sweep(pk, cases, torch, flush, stream)
+    steps_info = None
+    if not args.no_steps and rank == 0:
+        steps_info = run_step_configs(pk, cases, torch, stream)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -353,12 +356,37 @@ def run_ours(args, ws, rank, local):
             "config": workload_config(case) | {"parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
             "roofline": roofline, "rhs_roofline": rhs_roofline, "kernels": kern,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "gpu": torch.cuda.get_device_name(local), "sweep": sweep,
+            "gpu": torch.cuda.get_device_name(local), "sweep": sweep, "step_configs": steps_info,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def run_step_configs(pk, cases, torch, stream):
+    """C2-C4 (BASELINE configs[1..3]): the full averaged SSPRK3 run, device-resident (pswe_run)."""
+    out = []
+    for name in ("C2", "C3", "C4"):
+        c = cases.CASES[name]()
+        cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())
+        ctx = pk.integrator._prepare(c.state, cfg, c.params)
+        U0 = pk.dynamics.upload(ctx, c.state)
+        U = [x.clone() for x in U0]
+        ctx.run(c.dt, 1, U)  # warm-up (allocations, phase table)
+        torch.cuda.synchronize()
+        U = [x.clone() for x in U0]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        bad = ctx.run(c.dt, c.nsteps, U)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        units = 3 * c.nsteps * c.P * c.dof  # 3 averaged RHS per step
+        out.append({"config": name, "grid": c.grid.nx, "M": c.M, "P": c.P, "steps": c.nsteps,
+                    "run_ms": ms, "ms_per_step": ms / c.nsteps, "phase_dof_per_s": units / (ms * 1e-3),
+                    "nonfinite": bool(bad[0])})
+    return out
 
 
 def run_sweep(pk, cases, torch, flush, stream, steps=3):
@@ -413,6 +441,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-steps", action="store_true", help="skip the C2-C4 step-run timings")
     ap.add_argument("--chunk-mb", type=float, default=0.0, help="L2-resident chunk size (default: library's)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -93,7 +93,14 @@ struct pswe_ctx {
   size_t chunk_bytes = size_t(96) << 20;
   DevBuf<double2> inter, slots, Uc, Ac, Ac2;
   cudaStream_t st2 = nullptr;  // second chunk lane
+  // cached CUDA graph of one SSPRK3 step (pswe_run)
+  cudaGraphExec_t step_exec = nullptr;
+  double graph_dt = 0.0;
+  int64_t version = 0, graph_version = -1, step_graph_launches = 0;
+  const double2* graph_A = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t st_run = nullptr;  // pswe_run's stream (graph capture)
+  cudaEvent_t ev_run = nullptr;
   // phase tables (c1, c2)[p][j][r] of the exact route: one for the quadrature,
   // one for the single s = 0 node of apply_nonlinear; rebuilt when stale
   DevBuf<double2> ctab_q, ctab_0;
@@ -428,6 +435,40 @@ int decode_flags(int bits, int* stage, int* field) {
 
 const char* field_name(int f) { return f == 0 ? "u" : (f == 1 ? "v" : "eta"); }
 
+// Capture "step A -> B, copy B -> A" as a CUDA graph (cached per dt and
+// configuration version).  Every buffer it touches is allocated by the
+// un-captured first step, so nothing allocates during capture.
+int ensure_step_graph(pswe_ctx* c, double dt, Full3 Ain, Full3w Bout, size_t bytes3, cudaStream_t st) {
+  if (c->step_exec && c->graph_dt == dt && c->graph_version == c->version && c->graph_A == Ain.u) return PSWE_OK;
+  if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  c->step_exec = nullptr;
+  const bool prof = c->prof;
+  c->prof = false;
+  const int64_t l0 = c->launches;
+  CU(cudaStreamSynchronize(st));
+  CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+  int rc = step_impl(c, dt, Ain, Bout, st);
+  cudaError_t ce = cudaMemcpyAsync((void*)Ain.u, Bout.u, bytes3, cudaMemcpyDeviceToDevice, st);
+  cudaGraph_t g = nullptr;
+  cudaError_t ee = cudaStreamEndCapture(st, &g);
+  c->prof = prof;
+  if (rc != PSWE_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  CU(ce);
+  CU(ee);
+  cudaError_t ie = cudaGraphInstantiate(&c->step_exec, g, 0);
+  cudaGraphDestroy(g);
+  CU(ie);
+  c->step_graph_launches = c->launches - l0;
+  c->launches = l0;
+  c->graph_dt = dt;
+  c->graph_version = c->version;
+  c->graph_A = Ain.u;
+  return PSWE_OK;
+}
+
 }  // namespace
 
 // =============================================================== C ABI
@@ -511,6 +552,8 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
     }
   }
   if (cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st_run, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_run, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     pswe_destroy(c);
@@ -542,6 +585,9 @@ void pswe_destroy(pswe_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  if (c->ev_run) cudaEventDestroy(c->ev_run);
+  if (c->st_run) cudaStreamDestroy(c->st_run);
   delete c;
 }
 
@@ -556,6 +602,7 @@ int pswe_set_topography(pswe_ctx* c, const double* b_dev, void* stream) {
   pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p);
   c->launches++;
   CU(cudaMemcpyAsync(c->bc.p, c->Uc.p, (size_t)c->Ky * c->Kx * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  c->version++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
@@ -583,6 +630,7 @@ int pswe_set_quadrature(pswe_ctx* c, int n_nodes, const double* s, const double*
   CU(cudaMemcpy(c->s_dev.p, c->s_live.data(), P * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(c->w_dev.p, c->w_live.data(), P * sizeof(double), cudaMemcpyHostToDevice));
   c->quad_set = true;
+  c->version++;
   return PSWE_OK;
 }
 
@@ -600,6 +648,7 @@ int pswe_set_propagator(pswe_ctx* c, int kind, double Lambda, int n_poly, const 
   c->kind = kind;
   c->Lambda = Lambda;
   c->n_poly = n_poly;
+  c->version++;
   return PSWE_OK;
 }
 
@@ -722,18 +771,29 @@ int pswe_run(pswe_ctx* c, double dt, int nsteps, double* u, double* v, double* e
   if (check_cheb(c, dt, &msg) != PSWE_OK) return set_err(PSWE_EINVAL, "%s", msg.c_str());
   TRY(check_nodes(c));
   CU(cudaSetDevice(c->device));
-  cudaStream_t st = (cudaStream_t)stream;
+  // the run executes on the context's own stream (capturable even when the
+  // caller uses the legacy default stream), forked from / joined to `stream`
+  cudaStream_t ust = (cudaStream_t)stream;
+  cudaStream_t st = c->st_run;
+  CU(cudaEventRecord(c->ev_run, ust));
+  CU(cudaStreamWaitEvent(st, c->ev_run, 0));
   const size_t n = c->full_elems();
-  TRY(c->full_tmp.alloc(n * 15));
-  double2* A = c->full_tmp.p + 9 * n;
-  double2* B = c->full_tmp.p + 12 * n;
+  TRY(c->full_tmp.alloc(n * 18));
+  double2* A = c->full_tmp.p + 9 * n;   // state
+  double2* B = c->full_tmp.p + 12 * n;  // step output
+  double2* S = c->full_tmp.p + 15 * n;  // batch checkpoint
+  const size_t bytes3 = 3 * n * sizeof(double2);
   CU(cudaMemcpyAsync(A, u, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(A + n, v, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(A + 2 * n, e, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  const Full3 Ain{A, A + n, A + 2 * n};
+  const Full3w Bout{B, B + n, B + 2 * n};
+
+  // one checked step: A -> B -> A; returns 100 (and fills the outputs) on a non-finite stage
   int rc = PSWE_OK;
-  for (int i = 1; i <= nsteps; ++i) {
+  auto checked_step = [&](int i) -> int {
     CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
-    TRY(step_impl(c, dt, Full3{A, A + n, A + 2 * n}, Full3w{B, B + n, B + 2 * n}, st));
+    TRY(step_impl(c, dt, Ain, Bout, st));
     CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     int stage = 0, field = -1;
@@ -742,13 +802,50 @@ int pswe_run(pswe_ctx* c, double dt, int nsteps, double* u, double* v, double* e
       if (bad_stage) *bad_stage = stage;
       if (bad_field) *bad_field = field;
       rc = set_err(PSWE_ENONFINITE, "non-finite values in field %s after stage %d", field_name(field), stage);
-      break;
+      return 100;  // A still holds the state at the start of step i
     }
-    std::swap(A, B);
+    CU(cudaMemcpyAsync(A, B, bytes3, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  };
+
+  // step 1 un-captured (allocates every buffer, builds the phase table)
+  int i = 1;
+  {
+    const int r = checked_step(i);
+    if (r == 100) goto done;
+    if (r != PSWE_OK) return r;
+    ++i;
   }
+  // remaining steps: CUDA-graph replays of one step in batches, flags checked per batch
+  if (i <= nsteps) {
+    TRY(ensure_step_graph(c, dt, Ain, Bout, bytes3, st));
+    const int batch = 16;
+    while (i <= nsteps) {
+      const int k = std::min(batch, nsteps - i + 1);
+      CU(cudaMemcpyAsync(S, A, bytes3, cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
+      for (int j = 0; j < k; ++j) CU(cudaGraphLaunch(c->step_exec, st));
+      c->launches += (int64_t)k * c->step_graph_launches;
+      CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      if (*c->flags_host) {
+        // replay the batch step by step from its checkpoint to find the failing step
+        CU(cudaMemcpyAsync(A, S, bytes3, cudaMemcpyDeviceToDevice, st));
+        for (int j = 0; j < k; ++j) {
+          const int r = checked_step(i + j);
+          if (r == 100) goto done;
+          if (r != PSWE_OK) return r;
+        }
+      }
+      i += k;
+    }
+  }
+done:
   CU(cudaMemcpyAsync(u, A, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(v, A + n, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(e, A + 2 * n, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  CU(cudaEventRecord(c->ev_run, st));
+  CU(cudaStreamWaitEvent(ust, c->ev_run, 0));
   return rc;
 }
 
@@ -786,6 +883,7 @@ int pswe_profile_read(pswe_ctx* c, double* ms, int64_t* launches, int n) {
 int pswe_set_chunk_bytes(pswe_ctx* c, size_t bytes) {
   if (!c) return set_err(PSWE_EINVAL, "null context");
   c->chunk_bytes = std::max<size_t>(bytes, 1);
+  c->version++;
   return PSWE_OK;
 }
 

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
   const int tl = lane / T, t = lane % T;
   double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
   const size_t ostride = (size_t)5 * Ky;  // I1 row stride (one physical x)
+  const WLane wl = wlane<NX>(G.twx, t);
   int it = 0;
 #pragma unroll 1
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
@@ -181,15 +182,22 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
     const double s = ph.s[p0 + pl];
     mbar_wait(bar, it & 1);
     // e^{sL} per mode in place: (u, v, eta, b) -> (u', v', eta' - b) / (nx ny)
+    double kyb[GPW];
+#pragma unroll
+    for (int c = 0; c < GPW; ++c) kyb[c] = G.kyc[min(j0 + c, Ky - 1)];
     for (int idx = threadIdx.x; idx < ncol * Kx; idx += blockDim.x) {
       const int tt = idx / Kx, r = idx % Kx;
       double2* e = buf + idx;
       C3 q = {e[0], e[fs], e[2 * fs]};
       const double kx = kxs[r];
+      double ky = kyb[0];
+#pragma unroll
+      for (int c = 1; c < GPW; ++c)
+        if (tt == c) ky = kyb[c];
       if (tab)
-        q = exp_c12(e[4 * fs], q, G.ph, kx, G.kyc[j0 + tt]);
+        q = exp_c12(e[4 * fs], q, G.ph, kx, ky);
       else
-        q = expL(s, q, G.ph, kx, G.kyc[j0 + tt], pr);
+        q = expL(s, q, G.ph, kx, ky, pr);
       // slots 0..2 become u', v', eta' - b (the ikx fields are formed by the
       // consuming warps; writing them into slots 3/4 here raced with the
       // next block's TMA refill of those slots in testing)
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
     }
     __syncthreads();  // buffer consumed: refill it for the next block while the FFTs run
     if (f == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
-    wfft_t1<NX, true>(v, t, xb, G.twx);
+    wfft_t1<NX, true>(v, t, xb, wl);
     if (active) store_t1_strided<NX>(v, t, I + ((size_t)pl * NX * 5 + f) * Ky + j0 + tl, ostride);
   }
 }
@@ -390,6 +398,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
 
   double2 v[P];
   double pa[P];
+  const WLane wl = wlane<NY>(Gd.twy, t);
 #pragma unroll 1
   for (int it = 0; it < 4; ++it) {
     mbar_wait(bar, it & 1);
@@ -398,7 +407,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     // queue the next transform's inputs; they land while this one computes.
     // (No `continue` in this loop: nvcc 12.9 mis-carried pa[] across one.)
     if (it < 3) passB_prefetch<NY>(it + 1, lane, pre, bar, I, first_task, ntask, Ky);
-    wfft_t1<NY, true>(v, t, xb, Gd.twy);
+    wfft_t1<NY, true>(v, t, xb, wl);
     if (it == 0) {
 #pragma unroll
       for (int i = 0; i < P; ++i) uv[i * T + t] = v[i];
@@ -422,7 +431,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
       }
     }
     if (it < 2) continue;
-    wfft_t2<NY, false>(v, t, xb, Gd.twy);
+    wfft_t2<NY, false>(v, t, xb, wl);
     const int fo = it == 2 ? 0 : 2;
     unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
   }
@@ -499,6 +508,7 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
   double2* Ff = F + ((size_t)tl * 4 + f) * Kx;
   const double2* mine = pre + ((size_t)f * GPW + tl) * NX;
+  const WLane wl = wlane<NX>(G.twx, t);
   C3 acc[CPT];
 #pragma unroll
   for (int c = 0; c < CPT; ++c) acc[c] = c3zero();
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
 #pragma unroll
     for (int n1 = 0; n1 < P; ++n1) v[n1] = mine[t + T * n1];
     // the combine below reads ctb, so the refill waits for the end of this phase
-    wfft_t1<NX, false>(v, t, xb, G.twx);
+    wfft_t1<NX, false>(v, t, xb, wl);
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       const int r = band_r(t1_pos<NX>(t, i), NX, NX / 3, Kx);

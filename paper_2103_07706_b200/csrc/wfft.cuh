@@ -146,6 +146,29 @@ __device__ __forceinline__ double2 twg(const double2* __restrict__ tw, int e, bo
   return w;
 }
 
+// Per-lane twiddle bases (forward sign), loaded once per kernel instead of
+// once per transform: W_N^t (type 1 and type 2 for T <= 16), W_N^{n1} and
+// W_N^{2 n1} with n1 = t/2 (type 2, T == 32).
+struct WLane {
+  double2 wt, wn1, w2n1;
+};
+
+template <int N>
+__device__ __forceinline__ WLane wlane(const WTab tw, int t) {
+  WLane w;
+  if constexpr (N >= 32) {
+    w.wt = __ldg(tw.t0 + t);
+    w.wn1 = __ldg(tw.t0 + (t >> 1));
+    w.w2n1 = __ldg(tw.t0 + ((2 * (t >> 1)) & (N - 1)));
+  } else {
+    w.wt = w.wn1 = w.w2n1 = cmk(1.0, 0.0);
+    if constexpr (N >= 16) w.wt = __ldg(tw.t0 + t);
+  }
+  return w;
+}
+
+__device__ __forceinline__ double2 wsel(double2 w, bool inv) { return inv ? cmk(w.x, -w.y) : w; }
+
 // position held in register i by lane t after a type-1 transform (== type-2 input)
 template <int N>
 __device__ __forceinline__ int t1_pos(int t, int i) {
@@ -178,14 +201,14 @@ __device__ __forceinline__ int t1_pos(int t, int i) {
 // v[n1] = x[t + T n1] in; out per t1_pos.  xb: this transform's exchange buffer
 // (WF<N>::XBUF doubles); tw: global W_N^k table.
 template <int N, bool INV>
-__device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WTab tw) {
+__device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WLane& wl) {
   if constexpr (N == 8) {
     dft8<INV>(v);
   } else {
     constexpr int T = WF<N>::T, S = WF<N>::S;
     dft16<INV>(v);
     if constexpr (T > 1) {
-      apply_powers<16>(v, twg(tw.t0, t, INV));  // W_N^{t k1}
+      apply_powers<16>(v, wsel(wl.wt, INV));  // W_N^{t k1}
       if constexpr (T <= 16) {
         constexpr int C = 16 / T;
         PSWE_XPOSE(
@@ -224,7 +247,7 @@ __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WTa
 // ---- type 2 -------------------------------------------------------------------
 // input in t1_pos layout; out v[k2] = X[t + T k2].
 template <int N, bool INV>
-__device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WTab tw) {
+__device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLane& wl) {
   if constexpr (N == 8) {
     dft8<INV>(v);
   } else {
@@ -234,8 +257,9 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WTa
         constexpr int C = 16 / T;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          dftL<T, INV>(v + c * T);                                 // Z[n1][k1''], k1'' = 0..T-1
-          apply_powers<T>(v + c * T, twg(tw.t0, t + T * c, INV));  // W_N^{n1 k1''}
+          dftL<T, INV>(v + c * T);  // Z[n1][k1''], k1'' = 0..T-1
+          // W_N^{n1 k1''}, n1 = t + T c: base W_N^t W_16^c (N = 16 T)
+          apply_powers<T>(v + c * T, cmul(wsel(wl.wt, INV), w16(c, INV)));
         }
         PSWE_XPOSE(
             for (int c = 0; c < C; ++c) _Pragma("unroll") for (int k = 0; k < T; ++k) xb[(t + T * c) * S + k] = v[c * T + k].x,
@@ -243,7 +267,7 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WTa
             for (int n1 = 0; n1 < 16; ++n1) v[n1].x = xb[n1 * S + t],
             for (int n1 = 0; n1 < 16; ++n1) v[n1].y = xb[n1 * S + t])
       } else {
-        const int n1 = t >> 1, h = t & 1;
+        const int h = t & 1, n1 = t >> 1;
         // s_c = a + b, d_c = (a - b) W_32^c for this lane's c = 8h + cc
         double2 q[16];
 #pragma unroll
@@ -261,11 +285,11 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WTa
         dft16<INV>(q);  // Z[n1][2 q' + h]
         // twiddle W_N^{n1 (2q'+h)} = W^{n1 h} (W^{2 n1})^{q'}
         if (h) {
-          const double2 b1 = twg(tw.t0, n1, INV);
+          const double2 b1 = wsel(wl.wn1, INV);
 #pragma unroll
           for (int k = 0; k < 16; ++k) q[k] = cmul(q[k], b1);
         }
-        apply_powers<16>(q, twg(tw.t0, (2 * n1) & (N - 1), INV));
+        apply_powers<16>(q, wsel(wl.w2n1, INV));
         PSWE_XPOSE(
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].x,
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].y,

@@ -247,3 +247,35 @@ def test_native_code_is_what_ran():
     pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())
     assert ctx.launch_count > before
     assert _native._lib is not None
+
+
+def test_run_reports_failing_step_and_keeps_its_start_state():
+    """pswe_run (graph-batched) finds the exact failing step, like run()'s step loop (integrator.py:173-177)."""
+    c = cases.case_c1()
+    cfg = pk.StepConfig(dt=3600.0, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())
+    ctx = pk.integrator._prepare(c.state, cfg, c.params)
+    U = pk.dynamics.upload(ctx, c.state)
+    assert ctx.run(3600.0, 20, U) == (0, 0, -1)
+    # a huge state blows up after a few steps; the graph batch is replayed to locate the step
+    big = pk.State(grid=c.grid, u=c.state.u * 1e7, v=c.state.v, eta=c.state.eta * 1e7)
+    U = pk.dynamics.upload(ctx, big)
+    bad_step, stage, fld = ctx.run(3600.0, 40, U)
+    assert bad_step > 1 and stage in (1, 2, 3) and fld in (0, 1, 2)
+    # the returned state is the (finite) state at the start of the failing step
+    assert all(bool(t.isfinite().all()) for t in U)
+    U2 = pk.dynamics.upload(ctx, big)
+    assert ctx.run(3600.0, bad_step - 1, U2) == (0, 0, -1)
+    assert all(bool((a == b).all()) for a, b in zip(U, U2))
+
+
+def test_graph_batched_run_matches_single_steps_bitwise():
+    c = cases.case_c2()
+    cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())
+    ctx = pk.integrator._prepare(c.state, cfg, c.params)
+    U = pk.dynamics.upload(ctx, c.state)
+    ctx.run(c.dt, 20, U)
+    V = pk.dynamics.upload(ctx, c.state)
+    for _ in range(20):
+        V, (st, fl) = ctx.ssprk3_step(c.dt, V)
+        assert st == 0
+    assert all(bool((a == b).all()) for a, b in zip(U, V))
