@@ -129,7 +129,7 @@ double pswe_max_frequency(const pswe_ctx* ctx);
 /* Number of kernels this context has launched (instrumentation). */
 int64_t pswe_launch_count(const pswe_ctx* ctx);
 
-/* Tuning: bytes of chunk intermediates kept L2-resident (default 96 MiB per lane, two lanes). */
+/* Tuning: bytes of chunk intermediates per lane (default 768 MiB, two lanes). */
 int pswe_set_chunk_bytes(pswe_ctx* ctx, size_t bytes);
 
 /* Per-kernel CUDA-event timing (instrumentation for bench.py).  While

@@ -1,7 +1,9 @@
 // Bulk asynchronous global -> shared copies (TMA bulk engine, SASS UBLKCP)
-// completing on a shared-memory mbarrier.  Used to prefetch the next FFT's
-// input spectra while the current one computes.
+// and TMA tensor gathers (SASS UTMALDG) completing on a shared-memory
+// mbarrier.  Used to prefetch the next FFT's input while the current one
+// computes.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,6 +34,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA tensor load of one box of a rank-4 tensor map at coordinates
+// (c0, c1, c2, c3) (innermost first); dst must be 128-byte aligned.
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
 

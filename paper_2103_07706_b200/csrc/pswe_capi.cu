@@ -2,6 +2,7 @@
 // include/pswe_b200.h).  One context = one grid/physics on one device; it
 // owns the constant tables, the chunk intermediates and the stepper scratch.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -90,7 +91,7 @@ struct pswe_ctx {
   double Lambda = 0;
   DevBuf<double> a_dev;
   // scratch
-  size_t chunk_bytes = size_t(96) << 20;
+  size_t chunk_bytes = size_t(768) << 20;
   DevBuf<double2> inter, slots, Uc, Ac, Ac2;
   cudaStream_t st2 = nullptr;  // second chunk lane
   // cached CUDA graph of one SSPRK3 step (pswe_run)
@@ -186,14 +187,14 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
 }
 
 template <int NY>
-int launchB(pswe_ctx* c, int np, const double2* I1, double2* I2, cudaStream_t st) {
+int launchB(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cudaStream_t st) {
   using W = PassBW<NY>;
-  const size_t smem = W::bytes(c->Ky);
+  const size_t smem = W::bytes();
   auto kern = passB_kernel<NY>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, I1, I2);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, mI1, I2);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -209,7 +210,7 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
 }
 
 template <int NX>
-int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
+int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const CUtensorMap& mI2,
             double2* slots, cudaStream_t st) {
   using W = PassCW<NX>;
   const size_t smem = W::bytes(c->Kx);
@@ -218,7 +219,7 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   const int cols = (c->Ky + W::GPW - 1) / W::GPW;
   const int blocks = cols * Gc;
   ProfScope ps(c, 2, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, I2, c->ctab_cur, slots, first);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, mI2, c->ctab_cur, slots, first);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -236,15 +237,15 @@ int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
-int dispatchB(pswe_ctx* c, int np, const double2* I1, double2* I2, cudaStream_t st) {
+int dispatchB(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cudaStream_t st) {
   switch (c->ny) {
-    case 8: return launchB<8>(c, np, I1, I2, st);
-    case 16: return launchB<16>(c, np, I1, I2, st);
-    case 32: return launchB<32>(c, np, I1, I2, st);
-    case 64: return launchB<64>(c, np, I1, I2, st);
-    case 128: return launchB<128>(c, np, I1, I2, st);
-    case 256: return launchB<256>(c, np, I1, I2, st);
-    case 512: return launchB<512>(c, np, I1, I2, st);
+    case 8: return launchB<8>(c, np, mI1, I2, st);
+    case 16: return launchB<16>(c, np, mI1, I2, st);
+    case 32: return launchB<32>(c, np, mI1, I2, st);
+    case 64: return launchB<64>(c, np, mI1, I2, st);
+    case 128: return launchB<128>(c, np, mI1, I2, st);
+    case 256: return launchB<256>(c, np, mI1, I2, st);
+    case 512: return launchB<512>(c, np, mI1, I2, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported ny = %d", c->ny);
 }
@@ -260,18 +261,56 @@ int groupsC(const pswe_ctx* c, int CP) {
   }
 }
 
-int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
+int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const CUtensorMap& mI2,
               double2* slots, cudaStream_t st) {
   switch (c->nx) {
-    case 8: return launchC<8>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 16: return launchC<16>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 32: return launchC<32>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 64: return launchC<64>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 128: return launchC<128>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 256: return launchC<256>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 512: return launchC<512>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 8: return launchC<8>(c, ph, p0, np, Gc, first, mI2, slots, st);
+    case 16: return launchC<16>(c, ph, p0, np, Gc, first, mI2, slots, st);
+    case 32: return launchC<32>(c, ph, p0, np, Gc, first, mI2, slots, st);
+    case 64: return launchC<64>(c, ph, p0, np, Gc, first, mI2, slots, st);
+    case 128: return launchC<128>(c, ph, p0, np, Gc, first, mI2, slots, st);
+    case 256: return launchC<256>(c, ph, p0, np, Gc, first, mI2, slots, st);
+    case 512: return launchC<512>(c, ph, p0, np, Gc, first, mI2, slots, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
+}
+
+// TMA tensor map of a rank-4 fp64 tensor (dims innermost first, byte strides
+// of dims 1..3) with box `box`; the encoder comes from the driver through the
+// runtime's entry-point query, so the library links only against cudart.
+int encode_map(CUtensorMap* m, void* base, const cuuint64_t dims[4], const cuuint64_t strides[3],
+               const cuuint32_t box[4]) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q));
+    if (!enc || q != cudaDriverEntryPointSuccess)
+      return set_err(PSWE_ECUDA, "cuTensorMapEncodeTiled not available from the driver");
+  }
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(PSWE_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return PSWE_OK;
+}
+
+// I1[p][f][j][x] gathered by rows: box (re/im, 1 x, Ky j, 1 field-phase)
+int map_rows_I1(const pswe_ctx* c, double2* I1, int CP, CUtensorMap* m) {
+  const cuuint64_t nx = c->nx, Ky = c->Ky;
+  const cuuint64_t dims[4] = {2, nx, Ky, (cuuint64_t)5 * CP};
+  const cuuint64_t strides[3] = {16, nx * 16, Ky * nx * 16};
+  const cuuint32_t box[4] = {2, 1, (cuuint32_t)Ky, 1};
+  return encode_map(m, I1, dims, strides, box);
+}
+
+// I2[p][f][x][j] gathered by columns: box (re/im, 1 j, min(nx, 256) x, 1)
+int map_cols_I2(const pswe_ctx* c, double2* I2, int CP, CUtensorMap* m) {
+  const cuuint64_t nx = c->nx, Ky = c->Ky;
+  const cuuint64_t dims[4] = {2, Ky, nx, (cuuint64_t)4 * CP};
+  const cuuint64_t strides[3] = {16, Ky * 16, nx * Ky * 16};
+  const cuuint32_t box[4] = {2, 1, (cuuint32_t)std::min<cuuint64_t>(nx, 256), 1};
+  return encode_map(m, I2, dims, strides, box);
 }
 
 // Averaged RHS on compact data: chunks of phases through passes A, B, C,
@@ -325,6 +364,12 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     }
   }
   cudaStream_t lst[2] = {st, c->st2};
+  CUtensorMap mrow[2], mcol[2];
+  for (int L = 0; L < lanes; ++L) {
+    double2* I1 = c->inter.p + (size_t)L * per_phase * CP;
+    TRY(map_rows_I1(c, I1, CP, &mrow[L]));
+    TRY(map_cols_I2(c, I1 + (size_t)5 * c->Ky * c->nx * CP, CP, &mcol[L]));
+  }
   if (lanes == 2) {
     CU(cudaEventRecord(c->ev_fork, st));
     CU(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
@@ -337,8 +382,8 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     double2* I2 = I1 + (size_t)5 * c->Ky * c->nx * CP;
     double2* sl = c->slots.p + (size_t)L * Gc * c->compact_elems();
     TRY(dispatchA(c, ph, p0, np, Uc, I1, lst[L]));
-    TRY(dispatchB(c, np, I1, I2, lst[L]));
-    TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
+    TRY(dispatchB(c, np, mrow[L], I2, lst[L]));
+    TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, mcol[L], sl, lst[L]));
   }
   if (lanes == 2) {
     CU(cudaEventRecord(c->ev_join, c->st2));

@@ -8,11 +8,15 @@
 //             r = compact kx index 0..Kx-1 (wx = r for r <= KXM, r - Kx after).
 //             Only the 2/3 band |wx| <= nx/3, |wy| <= ny/3 (grid.py:102-103)
 //             is stored; the ky < 0 half is the conjugate mirror.
-//   I1 (pass A -> B): I1[p][x][f][j], p = phase in chunk, x = 0..nx-1
-//             (physical x), f in 0..4, j = 0..KYM (spectral y): one physical
-//             row's five half-spectra are contiguous for pass B.
-//   I2 (pass B -> C): I2[p][f][j][x], f in 0..3: one ky column contiguous
-//             for pass C.  Strided accesses are only ever stores (A, B).
+//   I1 (pass A -> B): I1[p][f][j][x], p = phase in chunk, f in 0..4,
+//             j = 0..KYM (spectral y), x = 0..nx-1 (physical x): each pass-A
+//             transform stores one contiguous column.
+//   I2 (pass B -> C): I2[p][f][x][j], f in 0..3: each pass-B transform
+//             stores one contiguous row.
+//   Every store is contiguous; the transposed reads are TMA tensor gathers
+//   (one box = one row of I1 / one column of I2, 16-byte elements) issued a
+//   transform ahead, so the strided side of each intermediate costs async
+//   L2 requests instead of partial-sector writes.
 //
 // Averaged RHS (averaging.py:116-156) for a chunk of phases:
 //   pass A  (per phase, ky column)  e^{sL} per mode + 5 inverse x-FFTs
@@ -53,11 +57,6 @@ __device__ __forceinline__ int band_r(int k, int n, int kxm, int Kx) {
   if (k <= kxm) return k;
   if (k >= n - kxm) return k - n + Kx;
   return -1;
-}
-
-// I[p][x][f][j]
-__device__ __forceinline__ size_t iidx(const GridDev& G, int pl, int x, int f, int j) {
-  return (((size_t)pl * G.nx + x) * 5 + f) * G.Ky + j;
 }
 
 __device__ __forceinline__ size_t cidx(const GridDev& G, int f, int j, int r) {
@@ -172,7 +171,6 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
 
   const int tl = lane / T, t = lane % T;
   double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
-  const size_t ostride = (size_t)5 * Ky;  // I1 row stride (one physical x)
   const WLane wl = wlane<NX>(G.twx, t);
   int it = 0;
 #pragma unroll 1
@@ -220,7 +218,7 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
     __syncthreads();  // buffer consumed: refill it for the next block while the FFTs run
     if (f == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
     wfft_t1<NX, true>(v, t, xb, wl);
-    if (active) store_t1_strided<NX>(v, t, I + ((size_t)pl * NX * 5 + f) * Ky + j0 + tl, ostride);
+    if (active) store_t1_strided<NX>(v, t, I + (((size_t)pl * 5 + f) * Ky + j0 + tl) * NX, 1);
   }
 }
 
@@ -239,12 +237,15 @@ struct PassBW {
   static constexpr int T = WF<NY>::T, P = WF<NY>::P, GPW = WF<NY>::GPW;
   static constexpr int WARPS = 4;
   static constexpr int GPC = WARPS * GPW;  // rows per CTA
-  // per warp: mbarrier | prefetch [GPW][2][Ky] | per group: xbuf, (u, v) stash
-  __host__ __device__ static size_t warp_bytes(int Ky) {
-    return 16 + (size_t)GPW * 2 * Ky * sizeof(double2) +
-           (size_t)GPW * (WF<NY>::XBUF * sizeof(double) + (size_t)P * T * sizeof(double2));
-  }
-  static size_t bytes(int Ky) { return (size_t)WARPS * ((warp_bytes(Ky) + 15) / 16 * 16) + (size_t)Ky * sizeof(double); }
+  static constexpr int Ky = NY / 3 + 1;
+  static constexpr int KYA = (Ky + 7) / 8 * 8;  // TMA destinations 128-byte aligned
+  // per warp (128-byte aligned): prefetch [GPW][2][KYA] | per group: xbuf,
+  // (u, v) stash | mbarrier;  then ky [Ky]
+  static constexpr size_t WARP_BYTES =
+      ((size_t)GPW * 2 * KYA * sizeof(double2) +
+       (size_t)GPW * (WF<NY>::XBUF * sizeof(double) + (size_t)P * T * sizeof(double2)) + 8 + 127) /
+      128 * 128;
+  static size_t bytes() { return (size_t)WARPS * WARP_BYTES + (size_t)Ky * sizeof(double); }
 };
 
 // type-1 input of the packed pair A + iB at position k = t + T*N1, from the
@@ -253,7 +254,7 @@ struct PassBW {
 // whose k range straddles a band edge.
 template <int NY, int N1, bool HAS_B, bool DERIV>
 __device__ __forceinline__ double2 pair_val(int t, const double2* pre, const double* kys) {
-  constexpr int T = WF<NY>::T, KYM = NY / 3, Ky = KYM + 1;
+  constexpr int T = WF<NY>::T, KYM = NY / 3;
   constexpr int kmin = T * N1, kmax = T * N1 + T - 1;
   if constexpr (kmin > KYM && kmax < NY - KYM) {
     return czero();
@@ -272,7 +273,7 @@ __device__ __forceinline__ double2 pair_val(int t, const double2* pre, const dou
     const double2 A = pre[jj];
     double2 B = czero();
     if constexpr (HAS_B) {
-      B = pre[Ky + jj];
+      B = pre[PassBW<NY>::KYA + jj];
       if constexpr (DERIV) B = cik(kys[jj], B);
     }
     if constexpr (N1 == 0) {
@@ -335,58 +336,58 @@ __device__ __forceinline__ void unpack_store(const double2* v, int t, double2* o
 __device__ __forceinline__ int passB_fa(int it) { return it == 0 ? 0 : (it == 1 ? 3 : (it == 2 ? 4 : 2)); }
 __device__ __forceinline__ int passB_fb(int it) { return it == 0 ? 1 : (it == 1 ? 0 : (it == 2 ? 1 : -1)); }
 
-// lane 0 of the warp queues the bulk copies of transform `it`'s inputs for the
-// warp's GPW rows into its prefetch buffer
+// Queue the TMA row gathers of transform `it`'s inputs for the warp's GPW
+// rows into its prefetch buffer: one box (1 x, Ky j) of I1 per field, at
+// tensor coordinates (0, x, 0, f + 5 p).  Lane 0 posts the byte count, lanes
+// 0..GPW-1 issue their row's gathers.
 template <int NY>
 __device__ __forceinline__ void passB_prefetch(int it, int lane, double2* pre, uint64_t* bar,
-                                               const double2* __restrict__ I, int first_task, int ntask,
-                                               int Ky) {
-  constexpr int GPW = WF<NY>::GPW;
+                                               const CUtensorMap* mI, int first_task, int ntask, int nx) {
+  constexpr int GPW = WF<NY>::GPW, KYA = PassBW<NY>::KYA;
+  constexpr uint32_t seg = (uint32_t)PassBW<NY>::Ky * sizeof(double2);
+  const int fa = passB_fa(it), fb = passB_fb(it);
   if (lane == 0) {
-    const int fa = passB_fa(it), fb = passB_fb(it);
-    const uint32_t seg = (uint32_t)Ky * sizeof(double2);
-    uint32_t bytes = 0;
-    for (int g = 0; g < GPW; ++g) {
-      const int task = first_task + g;
-      if (task >= ntask) break;
-      bytes += fb >= 0 ? 2 * seg : seg;
-    }
-    mbar_arrive_expect_tx(bar, bytes);
-    for (int g = 0; g < GPW; ++g) {
-      const int task = first_task + g;
-      if (task >= ntask) break;
-      const double2* row = I + (size_t)task * 5 * Ky;
-      bulk_g2s(pre + (size_t)g * 2 * Ky, row + (size_t)fa * Ky, seg, bar);
-      if (fb >= 0) bulk_g2s(pre + (size_t)g * 2 * Ky + Ky, row + (size_t)fb * Ky, seg, bar);
+    const int nrow = max(0, min(GPW, ntask - first_task));
+    mbar_arrive_expect_tx(bar, (uint32_t)nrow * (fb >= 0 ? 2 * seg : seg));
+  }
+  __syncwarp();
+  if (lane < GPW) {
+    const int task = first_task + lane;
+    if (task < ntask) {
+      const int p = task / nx, x = task % nx;
+      tma_load_4d(pre + (size_t)lane * 2 * KYA, mI, 0, x, 0, fa + 5 * p, bar);
+      if (fb >= 0) tma_load_4d(pre + (size_t)lane * 2 * KYA + KYA, mI, 0, x, 0, fb + 5 * p, bar);
     }
   }
 }
 
 template <int NY>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
-    passB_kernel(GridDev Gd, int np, const double2* __restrict__ I, double2* __restrict__ I2) {
+    passB_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, double2* __restrict__ I2) {
   using W = PassBW<NY>;
-  constexpr int T = W::T, P = W::P, GPW = W::GPW;
-  extern __shared__ __align__(16) unsigned char sbytes[];
-  constexpr int Ky = NY / 3 + 1;  // == Gd.Ky
+  constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA;
+  extern __shared__ __align__(128) unsigned char sbytes[];
+  constexpr int Ky = W::Ky;  // == Gd.Ky
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane % T, g = lane / T;
-  unsigned char* wbase = sbytes + (size_t)warp * ((W::warp_bytes(Ky) + 15) / 16 * 16);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wbase);
-  double2* pre = reinterpret_cast<double2*>(wbase + 16);             // [GPW][2][Ky]
-  double* xb = reinterpret_cast<double*>(pre + (size_t)GPW * 2 * Ky) + (size_t)g * WF<NY>::XBUF;
-  double2* uv = reinterpret_cast<double2*>(reinterpret_cast<double*>(pre + (size_t)GPW * 2 * Ky) +
+  unsigned char* wbase = sbytes + (size_t)warp * W::WARP_BYTES;
+  double2* pre = reinterpret_cast<double2*>(wbase);  // [GPW][2][KYA]
+  double* xb = reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) + (size_t)g * WF<NY>::XBUF;
+  double2* uv = reinterpret_cast<double2*>(reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) +
                                            (size_t)GPW * WF<NY>::XBUF) +
-                (size_t)g * P * T;                                      // [P][T]
+                (size_t)g * P * T;  // [P][T]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<double2*>(reinterpret_cast<double*>(
+                                                  pre + (size_t)GPW * 2 * KYA) + (size_t)GPW * WF<NY>::XBUF) +
+                                              (size_t)GPW * P * T);
   const int ntask = np * Gd.nx;
   const int first_task = (blockIdx.x * W::WARPS + warp) * GPW;
   const int task = first_task + g;
   const bool active = task < ntask;
   const int pl = active ? task / Gd.nx : 0, x = active ? task % Gd.nx : 0;
   const size_t KyNX = (size_t)Ky * Gd.nx;
-  double2* out = I2 + (size_t)pl * 4 * KyNX + x;  // I2[pl][f][j][x]
-  const double2* mypre = pre + (size_t)g * 2 * Ky;
-  double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * ((W::warp_bytes(Ky) + 15) / 16 * 16));
+  double2* out = I2 + (size_t)pl * 4 * KyNX + (size_t)x * Ky;  // I2[pl][f][x][j]
+  const double2* mypre = pre + (size_t)g * 2 * KYA;
+  double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * W::WARP_BYTES);
   for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
 
   if (lane == 0) {
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     fence_mbar_init();
   }
   __syncthreads();
-  passB_prefetch<NY>(0, lane, pre, bar, I, first_task, ntask, Ky);
+  passB_prefetch<NY>(0, lane, pre, bar, &mI, first_task, ntask, Gd.nx);
 
   double2 v[P];
   double pa[P];
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     __syncwarp();  // prefetch buffer consumed
     // queue the next transform's inputs; they land while this one computes.
     // (No `continue` in this loop: nvcc 12.9 mis-carried pa[] across one.)
-    if (it < 3) passB_prefetch<NY>(it + 1, lane, pre, bar, I, first_task, ntask, Ky);
+    if (it < 3) passB_prefetch<NY>(it + 1, lane, pre, bar, &mI, first_task, ntask, Gd.nx);
     wfft_t1<NY, true>(v, t, xb, wl);
     if (it == 0) {
 #pragma unroll
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     if (it < 2) continue;
     wfft_t2<NY, false>(v, t, xb, wl);
     const int fo = it == 2 ? 0 : 2;
-    unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
+    unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, 1, active);
   }
 }
 
@@ -449,10 +450,11 @@ struct PassCW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 4;
   static constexpr int CPT = 3;  // combine modes per thread (GPW * Kx <= 3 * 128)
-  // mbarrier | prefetch [4][GPW][NX] | (c1,c2) [GPW][Kx] | F [GPW][4][Kx] | xbuf per group | kx [Kx]
+  static constexpr int BOX = NX < 256 ? NX : 256;  // TMA box extent along x
+  // prefetch [4][GPW][NX] | (c1,c2) [GPW][Kx] | F [GPW][4][Kx] | xbuf per group | kx [Kx] | mbarrier
   static size_t bytes(int Kx) {
-    return 16 + (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * 5 * Kx * sizeof(double2) +
-           (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) + (size_t)Kx * sizeof(double);
+    return (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * 5 * Kx * sizeof(double2) +
+           (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) + (size_t)Kx * sizeof(double) + 8;
   }
 };
 
@@ -464,38 +466,44 @@ struct PassCW {
 // accumulators, which are added to the group's slot once at the end.
 template <int NX>
 __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
-    passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
+    passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const __grid_constant__ CUtensorMap mI2,
                  const double2* __restrict__ ctab, double2* __restrict__ slots, int first_chunk) {
   using W = PassCW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, CPT = W::CPT;
-  extern __shared__ __align__(16) unsigned char sbytes[];
+  extern __shared__ __align__(128) unsigned char sbytes[];
   constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
   const int Ky = G.Ky;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
-  double2* pre = reinterpret_cast<double2*>(sbytes + 16);  // [4][GPW][NX]
-  double2* ctb = pre + (size_t)4 * GPW * NX;                // [GPW][Kx]
-  double2* F = ctb + (size_t)GPW * Kx;                      // [GPW][4][Kx]
+  double2* pre = reinterpret_cast<double2*>(sbytes);  // [4][GPW][NX]
+  double2* ctb = pre + (size_t)4 * GPW * NX;           // [GPW][Kx]
+  double2* F = ctb + (size_t)GPW * Kx;                 // [GPW][4][Kx]
   double* xbuf = reinterpret_cast<double*>(F + (size_t)GPW * 4 * Kx);
   double* kxs = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(kxs + Kx);
   const int cols = (Ky + GPW - 1) / GPW;
   const int cb = blockIdx.x % cols, g = blockIdx.x / cols;
   const int lo = (int)(((long long)g * np) / Gc), hi = (int)(((long long)(g + 1) * np) / Gc);
-  const size_t KyKx = (size_t)Ky * Kx, KyNX = (size_t)Ky * NX;
+  const size_t KyKx = (size_t)Ky * Kx;
   const int j0 = cb * GPW;
   const int ncol = min(GPW, Ky - j0);  // active columns of this CTA (contiguous in I2)
   const bool tab = ctab != nullptr;
   const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < Kx; i += blockDim.x) kxs[i] = G.kxc[i];
 
-  // warp 0: lane 0 posts the byte count, lanes 0..4 each issue one bulk copy
+  // warp 0: lane 0 posts the byte count; the lanes issue the TMA column
+  // gathers (field f, column tl, x segment xs: one box of I2 at tensor
+  // coordinates (0, j0 + tl, xs * BOX, f + 4 pl)) and the phase-table copy
+  constexpr int NSEG = NX / W::BOX;
   auto prefetch = [&](int pl) {
     const uint32_t seg = (uint32_t)(ncol * NX * sizeof(double2));
     const uint32_t tseg = (uint32_t)(ncol * Kx * sizeof(double2));
     if (lane == 0) mbar_arrive_expect_tx(bar, 4 * seg + (tab ? tseg : 0));
     __syncwarp();
-    if (lane < 4)
-      bulk_g2s(pre + (size_t)lane * GPW * NX, I2 + ((size_t)pl * 4 + lane) * KyNX + (size_t)j0 * NX, seg, bar);
-    if (lane == 4 && tab) bulk_g2s(ctb, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg, bar);
+    for (int q = lane; q < 4 * ncol * NSEG; q += 32) {
+      const int ff = q / (ncol * NSEG), rem = q % (ncol * NSEG), tc = rem / NSEG, xs = rem % NSEG;
+      tma_load_4d(pre + ((size_t)ff * GPW + tc) * NX + xs * W::BOX, &mI2, 0, j0 + tc, xs * W::BOX, ff + 4 * pl,
+                  bar);
+    }
+    if (lane == 31 && tab) bulk_g2s(ctb, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg, bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
