@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
                  const double2* __restrict__ ctab, double2* __restrict__ I) {
   using W = PassAW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW;
-  extern __shared__ __align__(16) unsigned char sbytes[];
+  extern __shared__ __align__(128) unsigned char sbytes[];
   constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
   const int Ky = G.Ky;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
@@ -451,9 +451,10 @@ struct PassCW {
   static constexpr int WARPS = 4;
   static constexpr int CPT = 3;  // combine modes per thread (GPW * Kx <= 3 * 128)
   static constexpr int BOX = NX < 256 ? NX : 256;  // TMA box extent along x
-  // prefetch [4][GPW][NX] | (c1,c2) [GPW][Kx] | F [GPW][4][Kx] | xbuf per group | kx [Kx] | mbarrier
+  // prefetch [4][GPW][NX] (F [GPW][4][Kx] overlays it once the FFT inputs are
+  // in registers) | (c1,c2) [GPW][Kx] | xbuf per group | kx [Kx] | mbarrier
   static size_t bytes(int Kx) {
-    return (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * 5 * Kx * sizeof(double2) +
+    return (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * Kx * sizeof(double2) +
            (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) + (size_t)Kx * sizeof(double) + 8;
   }
 };
@@ -474,9 +475,9 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
   const int Ky = G.Ky;
   double2* pre = reinterpret_cast<double2*>(sbytes);  // [4][GPW][NX]
+  double2* F = pre;                                    // [GPW][4][Kx], overlays pre
   double2* ctb = pre + (size_t)4 * GPW * NX;           // [GPW][Kx]
-  double2* F = ctb + (size_t)GPW * Kx;                 // [GPW][4][Kx]
-  double* xbuf = reinterpret_cast<double*>(F + (size_t)GPW * 4 * Kx);
+  double* xbuf = reinterpret_cast<double*>(ctb + (size_t)GPW * Kx);
   double* kxs = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;
   uint64_t* bar = reinterpret_cast<uint64_t*>(kxs + Kx);
   const int cols = (Ky + GPW - 1) / GPW;
@@ -526,7 +527,8 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
     double2 v[P];
 #pragma unroll
     for (int n1 = 0; n1 < P; ++n1) v[n1] = mine[t + T * n1];
-    // the combine below reads ctb, so the refill waits for the end of this phase
+    __syncthreads();  // every warp holds its inputs: F may overwrite pre
+    // (the combine below reads F and ctb, so the refill waits for the end of this phase)
     wfft_t1<NX, false>(v, t, xb, wl);
 #pragma unroll
     for (int i = 0; i < P; ++i) {
