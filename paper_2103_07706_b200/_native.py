@@ -117,6 +117,73 @@ def _stream(torch):
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_PIN_OUT = {}
+_POOL = None
+
+
+def _copy_pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=3, thread_name_prefix="pswe-copy")
+    return _POOL
+
+
+def download_fields(tensors):
+    """CUDA tensors -> fresh numpy arrays: D2H into a reused pinned staging
+    buffer (one stream sync), then a host copy out of it."""
+    torch = _torch()
+    shape = tuple(tensors[0].shape)
+    key = (shape, tensors[0].dtype, len(tensors))
+    pin = _PIN_OUT.get(key)
+    if pin is None:
+        pin = torch.empty((len(tensors),) + shape, dtype=tensors[0].dtype, pin_memory=True)
+        _PIN_OUT[key] = pin
+    for i, t in enumerate(tensors):
+        pin[i].copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    pn = pin.numpy()
+    # fresh arrays fault their pages in on first write: copy the fields out in
+    # parallel threads (numpy releases the GIL for the copy)
+    return list(_copy_pool().map(lambda i: pn[i].copy(), range(len(tensors))))
+
+
+_PIN_IN = {}
+
+
+def upload_fields(arrays, device: int):
+    """Host fields -> CUDA tensors: parallel host copies into a reused pinned
+    staging buffer, then async H2D copies on the current stream.  The buffer
+    is rewritten only after the previous upload's copies completed."""
+    torch = _torch()
+    arrays = [np.asarray(a) for a in arrays]
+    shape = arrays[0].shape
+    key = (shape, len(arrays), device)
+    ent = _PIN_IN.get(key)
+    if ent is None:
+        pin = torch.empty((len(arrays),) + shape, dtype=torch.complex128, pin_memory=True)
+        ent = [pin, pin.numpy(), None]
+        _PIN_IN[key] = ent
+    pin, pn, ev = ent
+    if ev is not None:
+        ev.synchronize()
+
+    def put(i):
+        np.copyto(pn[i], arrays[i], casting="same_kind")
+
+    list(_copy_pool().map(put, range(len(arrays))))
+    dev = torch.device("cuda", device)
+    out = []
+    for i in range(len(arrays)):
+        t = torch.empty(shape, dtype=torch.complex128, device=dev)
+        t.copy_(pin[i], non_blocking=True)
+        out.append(t)
+    ev = torch.cuda.Event()
+    ev.record()
+    ent[2] = ev
+    return out
+
+
 class Context:
     """One grid + physics on one CUDA device (``pswe_ctx``).
 

@@ -112,11 +112,19 @@ def context(state_or_grid, params):
 
 
 def upload(ctx, state):
-    return [ctx.to_device(getattr(state, n)) for n in ("u", "v", "eta")]
+    fields = [getattr(state, n) for n in ("u", "v", "eta")]
+    if any(not isinstance(a, np.ndarray) for a in fields):
+        return [ctx.to_device(a) for a in fields]
+    for a in fields:
+        if a.shape != (ctx.nx, ctx.ny):
+            raise ValueError(f"field shape {a.shape} does not match the grid ({ctx.nx}, {ctx.ny})")
+    return _native.upload_fields(fields, ctx.device)
 
 
 def download(tensors):
-    return [t.cpu().numpy() for t in tensors]
+    if tensors and tensors[0].is_cuda:
+        return _native.download_fields(tensors)
+    return [t.numpy() for t in tensors]
 
 
 def rebuild(state, fields, t):
