@@ -186,18 +186,31 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
   return PSWE_OK;
 }
 
-template <int NY>
-int launchB(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cudaStream_t st) {
+// rows per pass-B CTA (the output tile width R) for transform length ny
+int passB_rows(int ny) { return 4 * 32 / std::max(1, ny / 16); }
+// tensor-memory stash + TMA tile store path: NY >= 64 and whole tiles per phase
+bool passB_fast(const pswe_ctx* c) { return c->ny >= 64 && c->nx % passB_rows(c->ny) == 0; }
+
+template <int NY, bool FAST>
+int launchB_t(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2, cudaStream_t st) {
   using W = PassBW<NY>;
-  const size_t smem = W::bytes();
-  auto kern = passB_kernel<NY>;
+  const size_t smem = W::template bytes<FAST>();
+  auto kern = passB_kernel<NY, FAST>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, mI1, I2);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, mI1, mO, I2);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
+}
+
+template <int NY>
+int launchB(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2, cudaStream_t st) {
+  if constexpr (NY >= 64) {
+    if (passB_fast(c)) return launchB_t<NY, true>(c, np, mI1, mO, I2, st);
+  }
+  return launchB_t<NY, false>(c, np, mI1, mO, I2, st);
 }
 
 template <int NX>
@@ -210,7 +223,7 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
 }
 
 template <int NX>
-int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const CUtensorMap& mI2,
+int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
             double2* slots, cudaStream_t st) {
   using W = PassCW<NX>;
   const size_t smem = W::bytes(c->Kx);
@@ -219,7 +232,7 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   const int cols = (c->Ky + W::GPW - 1) / W::GPW;
   const int blocks = cols * Gc;
   ProfScope ps(c, 2, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, mI2, c->ctab_cur, slots, first);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, I2, c->ctab_cur, slots, first);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -237,15 +250,15 @@ int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
-int dispatchB(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cudaStream_t st) {
+int dispatchB(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2, cudaStream_t st) {
   switch (c->ny) {
-    case 8: return launchB<8>(c, np, mI1, I2, st);
-    case 16: return launchB<16>(c, np, mI1, I2, st);
-    case 32: return launchB<32>(c, np, mI1, I2, st);
-    case 64: return launchB<64>(c, np, mI1, I2, st);
-    case 128: return launchB<128>(c, np, mI1, I2, st);
-    case 256: return launchB<256>(c, np, mI1, I2, st);
-    case 512: return launchB<512>(c, np, mI1, I2, st);
+    case 8: return launchB<8>(c, np, mI1, mO, I2, st);
+    case 16: return launchB<16>(c, np, mI1, mO, I2, st);
+    case 32: return launchB<32>(c, np, mI1, mO, I2, st);
+    case 64: return launchB<64>(c, np, mI1, mO, I2, st);
+    case 128: return launchB<128>(c, np, mI1, mO, I2, st);
+    case 256: return launchB<256>(c, np, mI1, mO, I2, st);
+    case 512: return launchB<512>(c, np, mI1, mO, I2, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported ny = %d", c->ny);
 }
@@ -261,16 +274,16 @@ int groupsC(const pswe_ctx* c, int CP) {
   }
 }
 
-int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const CUtensorMap& mI2,
+int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
               double2* slots, cudaStream_t st) {
   switch (c->nx) {
-    case 8: return launchC<8>(c, ph, p0, np, Gc, first, mI2, slots, st);
-    case 16: return launchC<16>(c, ph, p0, np, Gc, first, mI2, slots, st);
-    case 32: return launchC<32>(c, ph, p0, np, Gc, first, mI2, slots, st);
-    case 64: return launchC<64>(c, ph, p0, np, Gc, first, mI2, slots, st);
-    case 128: return launchC<128>(c, ph, p0, np, Gc, first, mI2, slots, st);
-    case 256: return launchC<256>(c, ph, p0, np, Gc, first, mI2, slots, st);
-    case 512: return launchC<512>(c, ph, p0, np, Gc, first, mI2, slots, st);
+    case 8: return launchC<8>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 16: return launchC<16>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 32: return launchC<32>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 64: return launchC<64>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 128: return launchC<128>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 256: return launchC<256>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 512: return launchC<512>(c, ph, p0, np, Gc, first, I2, slots, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
@@ -304,12 +317,13 @@ int map_rows_I1(const pswe_ctx* c, double2* I1, int CP, CUtensorMap* m) {
   return encode_map(m, I1, dims, strides, box);
 }
 
-// I2[p][f][x][j] gathered by columns: box (re/im, 1 j, min(nx, 256) x, 1)
-int map_cols_I2(const pswe_ctx* c, double2* I2, int CP, CUtensorMap* m) {
+// I2[p][f][j][x] written by pass-B tiles: box (re/im, R x, Ky j, 2 fields)
+int map_tiles_I2(const pswe_ctx* c, double2* I2, int CP, CUtensorMap* m) {
   const cuuint64_t nx = c->nx, Ky = c->Ky;
-  const cuuint64_t dims[4] = {2, Ky, nx, (cuuint64_t)4 * CP};
-  const cuuint64_t strides[3] = {16, Ky * 16, nx * Ky * 16};
-  const cuuint32_t box[4] = {2, 1, (cuuint32_t)std::min<cuuint64_t>(nx, 256), 1};
+  const cuuint64_t dims[4] = {2, nx, Ky, (cuuint64_t)4 * CP};
+  const cuuint64_t strides[3] = {16, nx * 16, Ky * nx * 16};
+  const cuuint32_t R = (cuuint32_t)std::min<cuuint64_t>(passB_rows(c->ny), nx);
+  const cuuint32_t box[4] = {2, R, (cuuint32_t)Ky, 2};
   return encode_map(m, I2, dims, strides, box);
 }
 
@@ -368,7 +382,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   for (int L = 0; L < lanes; ++L) {
     double2* I1 = c->inter.p + (size_t)L * per_phase * CP;
     TRY(map_rows_I1(c, I1, CP, &mrow[L]));
-    TRY(map_cols_I2(c, I1 + (size_t)5 * c->Ky * c->nx * CP, CP, &mcol[L]));
+    TRY(map_tiles_I2(c, I1 + (size_t)5 * c->Ky * c->nx * CP, CP, &mcol[L]));
   }
   if (lanes == 2) {
     CU(cudaEventRecord(c->ev_fork, st));
@@ -382,8 +396,8 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     double2* I2 = I1 + (size_t)5 * c->Ky * c->nx * CP;
     double2* sl = c->slots.p + (size_t)L * Gc * c->compact_elems();
     TRY(dispatchA(c, ph, p0, np, Uc, I1, lst[L]));
-    TRY(dispatchB(c, np, mrow[L], I2, lst[L]));
-    TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, mcol[L], sl, lst[L]));
+    TRY(dispatchB(c, np, mrow[L], mcol[L], I2, lst[L]));
+    TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
   }
   if (lanes == 2) {
     CU(cudaEventRecord(c->ev_join, c->st2));

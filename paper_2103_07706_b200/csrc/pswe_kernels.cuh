@@ -11,12 +11,13 @@
 //   I1 (pass A -> B): I1[p][f][j][x], p = phase in chunk, f in 0..4,
 //             j = 0..KYM (spectral y), x = 0..nx-1 (physical x): each pass-A
 //             transform stores one contiguous column.
-//   I2 (pass B -> C): I2[p][f][x][j], f in 0..3: each pass-B transform
-//             stores one contiguous row.
-//   Every store is contiguous; the transposed reads are TMA tensor gathers
-//   (one box = one row of I1 / one column of I2, 16-byte elements) issued a
-//   transform ahead, so the strided side of each intermediate costs async
-//   L2 requests instead of partial-sector writes.
+//   I2 (pass B -> C): I2[p][f][j][x], f in 0..3: one ky column contiguous
+//             for pass C's bulk copies.  A pass-B CTA stages the outputs of
+//             its R consecutive rows as a [f][j][R] tile in shared memory
+//             and writes it with one TMA tensor store (R x 16-byte runs).
+//   Pass A stores are contiguous; pass B reads its rows of I1 with TMA
+//   tensor gathers (one box = one row, 16-byte elements) issued a transform
+//   ahead.
 //
 // Averaged RHS (averaging.py:116-156) for a chunk of phases:
 //   pass A  (per phase, ky column)  e^{sL} per mode + 5 inverse x-FFTs
@@ -27,6 +28,7 @@
 // followed by an ordered reduction over the phase-group slots.
 #pragma once
 #include "async_copy.cuh"
+#include "tmem.cuh"
 #include "wfft.cuh"
 
 namespace pswe {
@@ -239,13 +241,27 @@ struct PassBW {
   static constexpr int GPC = WARPS * GPW;  // rows per CTA
   static constexpr int Ky = NY / 3 + 1;
   static constexpr int KYA = (Ky + 7) / 8 * 8;  // TMA destinations 128-byte aligned
-  // per warp (128-byte aligned): prefetch [GPW][2][KYA] | per group: xbuf,
-  // (u, v) stash | mbarrier;  then ky [Ky]
-  static constexpr size_t WARP_BYTES =
-      ((size_t)GPW * 2 * KYA * sizeof(double2) +
-       (size_t)GPW * (WF<NY>::XBUF * sizeof(double) + (size_t)P * T * sizeof(double2)) + 8 + 127) /
-      128 * 128;
-  static size_t bytes() { return (size_t)WARPS * WARP_BYTES + (size_t)Ky * sizeof(double); }
+  static constexpr int R = GPC;                 // rows per CTA (output tile width)
+  // FAST (NY >= 64 and R | nx): the (u, v) stash lives in tensor memory and
+  // the outputs leave through a shared [2][Ky][R] staging tile + TMA store.
+  // Otherwise (small grids) the stash is in shared memory and the outputs are
+  // stored directly.
+  // per warp (128-byte aligned): prefetch [GPW][2][KYA] | per group: xbuf
+  // [| (u, v) stash] | mbarrier;  then stage | ky [Ky] | TMEM base
+  template <bool FAST>
+  __host__ __device__ static constexpr size_t warp_bytes() {
+    return ((size_t)GPW * 2 * KYA * sizeof(double2) + (size_t)GPW * WF<NY>::XBUF * sizeof(double) +
+            (FAST ? 0 : (size_t)GPW * P * T * sizeof(double2)) + 8 + 127) /
+           128 * 128;
+  }
+  template <bool FAST>
+  __host__ __device__ static constexpr size_t stage_bytes() {
+    return FAST ? ((size_t)2 * Ky * R * sizeof(double2) + 127) / 128 * 128 : 0;
+  }
+  template <bool FAST>
+  static size_t bytes() {
+    return (size_t)WARPS * warp_bytes<FAST>() + stage_bytes<FAST>() + (size_t)Ky * sizeof(double) + 16;
+  }
 };
 
 // type-1 input of the packed pair A + iB at position k = t + T*N1, from the
@@ -361,40 +377,69 @@ __device__ __forceinline__ void passB_prefetch(int it, int lane, double2* pre, u
   }
 }
 
-template <int NY>
+// (u, v) of registers i0 .. i0+3 from the stash: tensor memory (FAST, four
+// loads in flight per wait) or shared memory
+template <int NY, bool FAST>
+__device__ __forceinline__ void uv_get4(double2 (&q)[4], const double2* uv, uint32_t taddr, int i0, int t) {
+  if constexpr (FAST) {
+    uint32_t r[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tmem_ld_x4(taddr + 4 * (i0 + k), r[k]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = tmem_unpack(r[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = uv[(i0 + k) * WF<NY>::T + t];
+  }
+}
+
+template <int NY, bool FAST>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
-    passB_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, double2* __restrict__ I2) {
+    passB_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mO,
+                 double2* __restrict__ I2) {
   using W = PassBW<NY>;
-  constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA;
+  constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA, R = W::R;
   extern __shared__ __align__(128) unsigned char sbytes[];
   constexpr int Ky = W::Ky;  // == Gd.Ky
+  constexpr size_t WB = W::template warp_bytes<FAST>();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane % T, g = lane / T;
-  unsigned char* wbase = sbytes + (size_t)warp * W::WARP_BYTES;
+  unsigned char* wbase = sbytes + (size_t)warp * WB;
   double2* pre = reinterpret_cast<double2*>(wbase);  // [GPW][2][KYA]
   double* xb = reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) + (size_t)g * WF<NY>::XBUF;
   double2* uv = reinterpret_cast<double2*>(reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) +
                                            (size_t)GPW * WF<NY>::XBUF) +
-                (size_t)g * P * T;  // [P][T]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<double2*>(reinterpret_cast<double*>(
-                                                  pre + (size_t)GPW * 2 * KYA) + (size_t)GPW * WF<NY>::XBUF) +
-                                              (size_t)GPW * P * T);
+                (size_t)g * P * T;  // [P][T] (small-grid path only)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + WB - 8);
+  double2* stage = reinterpret_cast<double2*>(sbytes + (size_t)W::WARPS * WB);  // [2][Ky][R] (FAST)
+  double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * WB + W::template stage_bytes<FAST>());
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kys + Ky);
   const int ntask = np * Gd.nx;
   const int first_task = (blockIdx.x * W::WARPS + warp) * GPW;
   const int task = first_task + g;
   const bool active = task < ntask;
   const int pl = active ? task / Gd.nx : 0, x = active ? task % Gd.nx : 0;
   const size_t KyNX = (size_t)Ky * Gd.nx;
-  double2* out = I2 + (size_t)pl * 4 * KyNX + (size_t)x * Ky;  // I2[pl][f][x][j]
+  double2* out = I2 + (size_t)pl * 4 * KyNX + x;  // I2[pl][f][j][x] (small-grid path)
+  const int rc = warp * GPW + g;                  // row within the CTA tile
   const double2* mypre = pre + (size_t)g * 2 * KYA;
-  double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * W::WARP_BYTES);
   for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
 
   if (lane == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
+  if constexpr (FAST) {
+    if (warp == 0) tmem_alloc(tslot, 128);
+    tmem_fence_before_sync();
+  }
   __syncthreads();
+  uint32_t taddr = 0;
+  if constexpr (FAST) {
+    tmem_fence_after_sync();
+    taddr = *tslot + ((uint32_t)(32 * warp) << 16);  // this warp's lane quadrant
+  }
   passB_prefetch<NY>(0, lane, pre, bar, &mI, first_task, ntask, Gd.nx);
 
   double2 v[P];
@@ -406,35 +451,86 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     build_pair<NY>(v, t, mypre, kys, it);
     __syncwarp();  // prefetch buffer consumed
     // queue the next transform's inputs; they land while this one computes.
-    // (No `continue` in this loop: nvcc 12.9 mis-carried pa[] across one.)
     if (it < 3) passB_prefetch<NY>(it + 1, lane, pre, bar, &mI, first_task, ntask, Gd.nx);
     wfft_t1<NY, true>(v, t, xb, wl);
     if (it == 0) {
+      if constexpr (FAST) {
+        tmem_stash16(taddr, v);
+        tmem_wait_st();
+      } else {
 #pragma unroll
-      for (int i = 0; i < P; ++i) uv[i * T + t] = v[i];
+        for (int i = 0; i < P; ++i) uv[i * T + t] = v[i];
+      }
     } else if (it == 1) {
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        const double2 q = uv[i * T + t];
-        pa[i] = -(q.x * v[i].x + q.y * v[i].y);  // A = -(u ux + v uy)
+      for (int i0 = 0; i0 < P; i0 += 4) {
+        double2 q[4];
+        uv_get4<NY, FAST>(q, uv, taddr, i0, t);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          pa[i0 + k] = -(q[k].x * v[i0 + k].x + q[k].y * v[i0 + k].y);  // A = -(u ux + v uy)
+      }
+      if constexpr (FAST) {  // park A in tensor memory across the next transform
+        tmem_stash16d(taddr + 64, pa);
+        tmem_wait_st();
       }
     } else if (it == 2) {
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        const double2 q = uv[i * T + t];
-        v[i] = cmk(pa[i], -(q.x * v[i].x + q.y * v[i].y));  // A + iB, B = -(u vx + v vy)
+      for (int i0 = 0; i0 < P; i0 += 4) {
+        double2 q[4];
+        uv_get4<NY, FAST>(q, uv, taddr, i0, t);
+        double a4[4];
+        if constexpr (FAST) {
+          uint32_t r[8];
+          tmem_ld_x8(taddr + 64 + 2 * i0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) a4[k] = __hiloint2double(r[2 * k + 1], r[2 * k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) a4[k] = pa[i0 + k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // A + iB, B = -(u vx + v vy)
+          v[i0 + k] = cmk(a4[k], -(q[k].x * v[i0 + k].x + q[k].y * v[i0 + k].y));
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        const double2 q = uv[i * T + t];
-        v[i] = cmk(q.x * v[i].x, q.y * v[i].x);  // C + iD = u depth + i v depth
+      for (int i0 = 0; i0 < P; i0 += 4) {
+        double2 q[4];
+        uv_get4<NY, FAST>(q, uv, taddr, i0, t);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // C + iD = u depth + i v depth
+          v[i0 + k] = cmk(q[k].x * v[i0 + k].x, q[k].y * v[i0 + k].x);
       }
     }
     if (it < 2) continue;
     wfft_t2<NY, false>(v, t, xb, wl);
     const int fo = it == 2 ? 0 : 2;
-    unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, 1, active);
+    if constexpr (FAST) {
+      // the previous tile store has finished reading the staging tile
+      if (threadIdx.x == 0) bulk_wait_read0();
+      __syncthreads();
+      unpack_store<NY>(v, t, stage + rc, stage + (size_t)Ky * R + rc, Ky, R, true);
+      fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int t0 = blockIdx.x * R;  // first row of the tile (one phase)
+        tma_store_4d(&mO, 0, t0 % Gd.nx, 0, 4 * (t0 / Gd.nx) + fo, stage);
+        bulk_commit();
+      }
+    } else {
+      unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
+    }
+  }
+  if constexpr (FAST) {
+    if (threadIdx.x == 0) bulk_wait0();
+    tmem_fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+      tmem_fence_after_sync();
+      tmem_dealloc(*tslot, 128);
+    }
   }
 }
 
@@ -450,7 +546,6 @@ struct PassCW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 4;
   static constexpr int CPT = 3;  // combine modes per thread (GPW * Kx <= 3 * 128)
-  static constexpr int BOX = NX < 256 ? NX : 256;  // TMA box extent along x
   // prefetch [4][GPW][NX] (F [GPW][4][Kx] overlays it once the FFT inputs are
   // in registers) | (c1,c2) [GPW][Kx] | xbuf per group | kx [Kx] | mbarrier
   static size_t bytes(int Kx) {
@@ -467,7 +562,7 @@ struct PassCW {
 // accumulators, which are added to the group's slot once at the end.
 template <int NX>
 __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
-    passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const __grid_constant__ CUtensorMap mI2,
+    passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
                  const double2* __restrict__ ctab, double2* __restrict__ slots, int first_chunk) {
   using W = PassCW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, CPT = W::CPT;
@@ -490,21 +585,17 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < Kx; i += blockDim.x) kxs[i] = G.kxc[i];
 
-  // warp 0: lane 0 posts the byte count; the lanes issue the TMA column
-  // gathers (field f, column tl, x segment xs: one box of I2 at tensor
-  // coordinates (0, j0 + tl, xs * BOX, f + 4 pl)) and the phase-table copy
-  constexpr int NSEG = NX / W::BOX;
+  // warp 0: lane 0 posts the byte count, lanes 0..4 each issue one bulk copy
+  // (the CTA's ncol columns of field f are contiguous in I2)
+  const size_t KyNX = (size_t)Ky * NX;
   auto prefetch = [&](int pl) {
     const uint32_t seg = (uint32_t)(ncol * NX * sizeof(double2));
     const uint32_t tseg = (uint32_t)(ncol * Kx * sizeof(double2));
     if (lane == 0) mbar_arrive_expect_tx(bar, 4 * seg + (tab ? tseg : 0));
     __syncwarp();
-    for (int q = lane; q < 4 * ncol * NSEG; q += 32) {
-      const int ff = q / (ncol * NSEG), rem = q % (ncol * NSEG), tc = rem / NSEG, xs = rem % NSEG;
-      tma_load_4d(pre + ((size_t)ff * GPW + tc) * NX + xs * W::BOX, &mI2, 0, j0 + tc, xs * W::BOX, ff + 4 * pl,
-                  bar);
-    }
-    if (lane == 31 && tab) bulk_g2s(ctb, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg, bar);
+    if (lane < 4)
+      bulk_g2s(pre + (size_t)lane * GPW * NX, I2 + ((size_t)pl * 4 + lane) * KyNX + (size_t)j0 * NX, seg, bar);
+    if (lane == 4 && tab) bulk_g2s(ctb, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg, bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);

@@ -11,18 +11,37 @@ using namespace pswe;
 
 constexpr int NX = 512, KY = 171, NF = 5, NP = 8;
 
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // it: fields (0,1) (3,0) (4,1) (2,-)
 __device__ int fa_of(int it) { return it == 0 ? 0 : (it == 1 ? 3 : (it == 2 ? 4 : 2)); }
 __device__ int fb_of(int it) { return it == 0 ? 1 : (it == 1 ? 0 : (it == 2 ? 1 : -1)); }
+
+// cp.async (LDGSTS) gather: lanes copy the row's 16-byte elements themselves
+__global__ void __launch_bounds__(128) rows_ldgsts(const double2* I, double* out) {
+  __shared__ __align__(128) double2 pre[4][2][176];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc = 0;
+  const int ntask = NP * NX;
+  for (int task = blockIdx.x * 4 + warp; task < ntask; task += gridDim.x * 4) {
+    const int p = task / NX, x = task % NX;
+    for (int it = 0; it < 4; ++it) {
+      const int fa = fa_of(it), fb = fb_of(it);
+      const double2* ga = I + ((size_t)(p * NF + fa) * KY) * NX + x;
+      for (int j = lane; j < KY; j += 32) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&pre[warp][0][j])), "l"(ga + (size_t)j * NX) : "memory");
+      }
+      if (fb >= 0) {
+        const double2* gb = I + ((size_t)(p * NF + fb) * KY) * NX + x;
+        for (int j = lane; j < KY; j += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&pre[warp][1][j])), "l"(gb + (size_t)j * NX) : "memory");
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      for (int j = lane; j < KY; j += 32) acc += pre[warp][0][j].x + pre[warp][1][j].y;
+      __syncwarp();
+    }
+  }
+  out[blockIdx.x * 128 + threadIdx.x] = acc;
+}
 
 template <bool GATHER>
 __global__ void __launch_bounds__(128) rows_kernel(const __grid_constant__ CUtensorMap map, const double2* I, double* out) {
@@ -84,11 +103,12 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   for (int grid : {148 * 3, 148 * 6, 148 * 12}) {
-    for (int g = 0; g < 2; ++g) {
+    for (int g = 0; g < 3; ++g) {
       float best = 1e9;
       for (int rep = 0; rep < 5; ++rep) {
         cudaEventRecord(a);
-        if (g) rows_kernel<true><<<grid, 128>>>(map, I, out);
+        if (g == 1) rows_kernel<true><<<grid, 128>>>(map, I, out);
+        else if (g == 2) rows_ldgsts<<<grid, 128>>>(I, out);
         else rows_kernel<false><<<grid, 128>>>(map, I, out);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
@@ -97,7 +117,7 @@ int main() {
         if (ms < best) best = ms;
       }
       const double bytes = (double)NP * NX * 7 * KY * 16;
-      printf("grid %d %s: %.3f us  %.1f GB/s  (%.2f us per phase)\n", grid, g ? "tensor-gather" : "bulk-contig", best * 1e3,
+      printf("grid %d %s: %.3f us  %.1f GB/s  (%.2f us per phase)\n", grid, g == 1 ? "tensor-gather" : (g == 2 ? "ldgsts-gather" : "bulk-contig"), best * 1e3,
              bytes / (best * 1e-3) / 1e9, best * 1e3 / NP);
     }
   }
