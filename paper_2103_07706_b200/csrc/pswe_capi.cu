@@ -93,7 +93,10 @@ struct pswe_ctx {
   // scratch
   size_t chunk_bytes = size_t(768) << 20;
   DevBuf<double2> inter, slots, Uc, Ac, Ac2;
-  cudaStream_t st2 = nullptr;  // second chunk lane
+  static constexpr int MAX_LANES = 4;
+  cudaStream_t st_lane[MAX_LANES - 1] = {};  // chunk lanes 1.. (lane 0 is the caller's stream)
+  cudaEvent_t ev_lane[MAX_LANES - 1] = {};
+  int n_lanes = 3;
   // cached CUDA graph of one SSPRK3 step (pswe_run)
   cudaGraphExec_t step_exec = nullptr;
   double graph_dt = 0.0;
@@ -356,7 +359,8 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   // slot accumulates its lane's chunks in order and the final reduction sums
   // lane 0's slots then lane 1's -- a fixed order, so results stay bitwise
   // deterministic.
-  const int lanes = (P > CP) ? 2 : 1;
+  const int nchunks = (P + CP - 1) / CP;
+  const int lanes = std::max(1, std::min(c->n_lanes, nchunks));
   TRY(c->inter.alloc(per_phase * CP * lanes));
   TRY(c->slots.alloc((size_t)lanes * Gc * c->compact_elems()));
   if (getenv("PSWE_DEBUG_POISON")) {  // debug: NaN-fill intermediates to expose unwritten entries
@@ -377,16 +381,16 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
       ph.uniform = 1;  // a single phase: the rotor is only anchored, never advanced
     }
   }
-  cudaStream_t lst[2] = {st, c->st2};
-  CUtensorMap mrow[2], mcol[2];
+  cudaStream_t lst[pswe_ctx::MAX_LANES] = {st, c->st_lane[0], c->st_lane[1], c->st_lane[2]};
+  CUtensorMap mrow[pswe_ctx::MAX_LANES], mcol[pswe_ctx::MAX_LANES];
   for (int L = 0; L < lanes; ++L) {
     double2* I1 = c->inter.p + (size_t)L * per_phase * CP;
     TRY(map_rows_I1(c, I1, CP, &mrow[L]));
     TRY(map_tiles_I2(c, I1 + (size_t)5 * c->Ky * c->nx * CP, CP, &mcol[L]));
   }
-  if (lanes == 2) {
+  if (lanes > 1) {
     CU(cudaEventRecord(c->ev_fork, st));
-    CU(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+    for (int L = 1; L < lanes; ++L) CU(cudaStreamWaitEvent(lst[L], c->ev_fork, 0));
   }
   int chunk = 0;
   for (int p0 = 0; p0 < P; p0 += CP, ++chunk) {
@@ -399,9 +403,9 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     TRY(dispatchB(c, np, mrow[L], mcol[L], I2, lst[L]));
     TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
   }
-  if (lanes == 2) {
-    CU(cudaEventRecord(c->ev_join, c->st2));
-    CU(cudaStreamWaitEvent(st, c->ev_join, 0));
+  for (int L = 1; L < lanes; ++L) {
+    CU(cudaEventRecord(c->ev_lane[L - 1], lst[L]));
+    CU(cudaStreamWaitEvent(st, c->ev_lane[L - 1], 0));
   }
   const size_t n = c->compact_elems();
   ProfScope ps(c, 3, st);
@@ -610,8 +614,15 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
       return rc;
     }
   }
-  if (cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->st_run, cudaStreamNonBlocking) != cudaSuccess ||
+  for (int L = 0; L < pswe_ctx::MAX_LANES - 1; ++L) {
+    if (cudaStreamCreateWithFlags(&c->st_lane[L], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_lane[L], cudaEventDisableTiming) != cudaSuccess) {
+      pswe_destroy(c);
+      return set_err(PSWE_ECUDA, "stream/event creation failed");
+    }
+  }
+  if (const char* e = getenv("PSWE_LANES")) c->n_lanes = std::max(1, std::min(pswe_ctx::MAX_LANES, atoi(e)));
+  if (cudaStreamCreateWithFlags(&c->st_run, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_run, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -643,7 +654,10 @@ void pswe_destroy(pswe_ctx* c) {
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->st2) cudaStreamDestroy(c->st2);
+  for (int L = 0; L < pswe_ctx::MAX_LANES - 1; ++L) {
+    if (c->ev_lane[L]) cudaEventDestroy(c->ev_lane[L]);
+    if (c->st_lane[L]) cudaStreamDestroy(c->st_lane[L]);
+  }
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   if (c->ev_run) cudaEventDestroy(c->ev_run);
   if (c->st_run) cudaStreamDestroy(c->st_run);
