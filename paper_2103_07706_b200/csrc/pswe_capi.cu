@@ -218,11 +218,24 @@ int launchB(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, 
 
 template <int NX>
 int pass_c_groups(const pswe_ctx* c, int CP) {
-  // enough CTAs for ~4 per SM, each looping over CP/Gc phases
+  // phase groups per chunk: the grid (cols x Gc CTAs) should fill whole waves
+  // of the 3 x 148 resident CTAs, each CTA keeping >= 4 phases to amortise its
+  // prologue and slot update.  Pick the Gc with the best wave efficiency.
   const int cols = (c->Ky + PassCW<NX>::GPW - 1) / PassCW<NX>::GPW;
-  int want = (3 * 148 + cols - 1) / cols;
-  if (const char* e = getenv("PSWE_GC")) want = atoi(e);  // tuning experiments
-  return std::max(1, std::min(want, CP));
+  const int slots = 3 * 148;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int g = 1; g <= std::max(1, CP / 4) && g <= 16; ++g) {
+    const int ctas = cols * g;
+    const int waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / ((double)waves * slots);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = g;
+    }
+  }
+  if (const char* e = getenv("PSWE_GC")) best = atoi(e);  // tuning experiments
+  return std::max(1, std::min(best, CP));
 }
 
 template <int NX>
