@@ -45,6 +45,30 @@ __device__ __forceinline__ void dft4(double2& y0, double2& y1, double2& y2, doub
   y3 = csub(d0, r);
 }
 
+// dft4 with y2 == 0 (known at compile time): s0 = d0 = y0
+template <bool INV>
+__device__ __forceinline__ void dft4_z2(double2& y0, double2& y1, double2& y2, double2& y3) {
+  const double2 s1 = cadd(y1, y3), d1 = csub(y1, y3);
+  const double2 r = INV ? cmk(-d1.y, d1.x) : cmk(d1.y, -d1.x);
+  const double2 a = y0;
+  y0 = cadd(a, s1);
+  y2 = csub(a, s1);
+  y1 = cadd(a, r);
+  y3 = csub(a, r);
+}
+
+// dft4 with y1 == 0: s1 = y3, d1 = -y3
+template <bool INV>
+__device__ __forceinline__ void dft4_z1(double2& y0, double2& y1, double2& y2, double2& y3) {
+  const double2 s0 = cadd(y0, y2), d0 = csub(y0, y2);
+  // r = (-/+ i) * d1 with d1 = -y3
+  const double2 r = INV ? cmk(y3.y, -y3.x) : cmk(-y3.y, y3.x);
+  y0 = cadd(s0, y3);
+  y2 = csub(s0, y3);
+  y1 = cadd(d0, r);
+  y3 = csub(d0, r);
+}
+
 template <bool INV>
 __device__ __forceinline__ void dft8(double2* v) {
   const double c = 0.70710678118654752440;  // sqrt(1/2)

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
     }
     __syncthreads();  // buffer consumed: refill it for the next block while the FFTs run
     if (f == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
-    wfft_t1<NX, true>(v, t, xb, wl);
+    wfft_t1<NX, true, true>(v, t, xb, wl);
     if (active) store_t1_strided<NX>(v, t, I + (((size_t)pl * 5 + f) * Ky + j0 + tl) * NX, 1);
   }
 }
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     __syncwarp();  // prefetch buffer consumed
     // queue the next transform's inputs; they land while this one computes.
     if (it < 3) passB_prefetch<NY>(it + 1, lane, pre, bar, &mI, first_task, ntask, Gd.nx);
-    wfft_t1<NY, true>(v, t, xb, wl);
+    wfft_t1<NY, true, true>(v, t, xb, wl);
     if (it == 0) {
       if constexpr (FAST) {
         tmem_stash16(taddr, v);

@@ -68,14 +68,23 @@ __device__ __forceinline__ double2 w32(int e, bool inv) {
 }
 __device__ __forceinline__ double2 w16(int e, bool inv) { return w32(2 * e, inv); }
 
-// natural-order 16-point DFT in registers: 4 x 4 Cooley-Tukey
-template <bool INV>
+// natural-order 16-point DFT in registers: 4 x 4 Cooley-Tukey.  BAND: the
+// inputs v[6..9] are known zeros (2/3-truncated spectra entering an inverse
+// transform of length >= 64), so each first-layer dft4 has one zero input.
+template <bool INV, bool BAND = false>
 __device__ __forceinline__ void dft16(double2* v) {
   double2 a[4][4];  // a[n2][k1]
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) {
     double2 y0 = v[n2], y1 = v[n2 + 4], y2 = v[n2 + 8], y3 = v[n2 + 12];
-    dft4<INV>(y0, y1, y2, y3);
+    if constexpr (BAND) {
+      if (n2 < 2)
+        dft4_z2<INV>(y0, y1, y2, y3);  // y2 = v[8], v[9]
+      else
+        dft4_z1<INV>(y0, y1, y2, y3);  // y1 = v[6], v[7]
+    } else {
+      dft4<INV>(y0, y1, y2, y3);
+    }
     a[n2][0] = y0;
     a[n2][1] = y1;
     a[n2][2] = y2;
@@ -200,13 +209,16 @@ __device__ __forceinline__ int t1_pos(int t, int i) {
 // ---- type 1 -------------------------------------------------------------------
 // v[n1] = x[t + T n1] in; out per t1_pos.  xb: this transform's exchange buffer
 // (WF<N>::XBUF doubles); tw: global W_N^k table.
-template <int N, bool INV>
+// BAND: input registers 6..9 hold out-of-band (zero) positions, true for a
+// 2/3-truncated spectrum when N >= 64 (positions t + T n1, n1 = 6..9, all lie
+// strictly between N/3 and N - N/3).
+template <int N, bool INV, bool BAND = false>
 __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WLane& wl) {
   if constexpr (N == 8) {
     dft8<INV>(v);
   } else {
     constexpr int T = WF<N>::T, S = WF<N>::S;
-    dft16<INV>(v);
+    dft16<INV, BAND && (N >= 64)>(v);
     if constexpr (T > 1) {
       apply_powers<16>(v, wsel(wl.wt, INV));  // W_N^{t k1}
       if constexpr (T <= 16) {
