@@ -129,7 +129,15 @@ double pswe_max_frequency(const pswe_ctx* ctx);
 /* Number of kernels this context has launched (instrumentation). */
 int64_t pswe_launch_count(const pswe_ctx* ctx);
 
-/* Tuning: bytes of chunk intermediates per lane (default 768 MiB, two lanes). */
+/* Snapshot diagnostics of a full-layout state (Trajectory.record,
+ * integrator.py:124-135, and energy_mass, diagnostics.py:58-78): physical
+ * fields by a full 2-D C2R on the device (Hermitian part, as real(ifft2)),
+ * then out3_host = {energy, mass, max speed}.  Uses the topography last set
+ * with pswe_set_topography (zero if never set).  Synchronises the stream. */
+int pswe_diagnostics(pswe_ctx* ctx, const double* u_dev, const double* v_dev, const double* eta_dev,
+                     double* out3_host, void* stream);
+
+/* Tuning: bytes of chunk intermediates per lane (default 768 MiB, three lanes). */
 int pswe_set_chunk_bytes(pswe_ctx* ctx, size_t bytes);
 
 /* Per-kernel CUDA-event timing (instrumentation for bench.py).  While

@@ -54,6 +54,7 @@ SIGNATURES = {
     "pswe_run": (_i, [_vp, _d, _i, _vp, _vp, _vp, _c_int_p, _c_int_p, _c_int_p, _vp]),
     "pswe_max_frequency": (_d, [_vp]),
     "pswe_launch_count": (ctypes.c_int64, [_vp]),
+    "pswe_diagnostics": (_i, [_vp, _vp, _vp, _vp, ctypes.POINTER(_d), _vp]),
     "pswe_set_chunk_bytes": (_i, [_vp, ctypes.c_size_t]),
     "pswe_profile_enable": (_i, [_vp, _i]),
     "pswe_profile_read": (_i, [_vp, ctypes.POINTER(_d), ctypes.POINTER(ctypes.c_int64), _i]),
@@ -340,6 +341,12 @@ class Context:
             return out, (st.value, fl.value)
         _check(rc)
         return out, (0, -1)
+
+    def diagnostics(self, U) -> tuple[float, float, float]:
+        """(energy, mass, max speed) of a full-layout state on the device."""
+        out = (ctypes.c_double * 3)()
+        _check(_lib.pswe_diagnostics(self.h, *(_dptr(x) for x in U), out, _stream(self.torch)))
+        return float(out[0]), float(out[1]), float(out[2])
 
     def run(self, dt: float, nsteps: int, U):
         """In-place nsteps on U (list of 3 tensors). Returns (bad_step, stage, field)."""

@@ -15,6 +15,7 @@
 
 #include "../../include/pswe_b200.h"
 #include "pswe_kernels.cuh"
+#include "diag_kernels.cuh"
 
 using namespace pswe;
 
@@ -78,6 +79,8 @@ struct pswe_ctx {
   std::vector<double> kx_full, ky_full;
   DevBuf<double> kxc, kyc, kxf, kyf;
   DevBuf<double2> twx, twy, bc;
+  DevBuf<double2> bfull, diag_cols;  // full-layout topography; diagnostics scratch
+  DevBuf<double> diag_part;
   // quadrature (live nodes only)
   std::vector<double> s_live, w_live;
   std::vector<int> k_live;
@@ -302,6 +305,25 @@ int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first
     case 512: return launchC<512>(c, ph, p0, np, Gc, first, I2, slots, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
+}
+
+template <int NX>
+int launch_diag_cols(pswe_ctx* c, const double2* u, const double2* v, const double2* e, const double2* b,
+                     cudaStream_t st) {
+  const int tasks = 4 * (c->ny / 2 + 1), per = 4 * WF<NX>::GPW;
+  diag_cols_kernel<NX><<<(tasks + per - 1) / per, 128, 0, st>>>(c->grid(), u, v, e, b, c->diag_cols.p);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+template <int NY>
+int launch_diag_rows(pswe_ctx* c, cudaStream_t st) {
+  const int per = 4 * WF<NY>::GPW;
+  diag_rows_kernel<NY><<<(c->nx + per - 1) / per, 128, 0, st>>>(c->grid(), c->diag_cols.p, c->H, c->g,
+                                                                  c->diag_part.p);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
 }
 
 // TMA tensor map of a rank-4 fp64 tensor (dims innermost first, byte strides
@@ -660,8 +682,10 @@ void pswe_destroy(pswe_ctx* c) {
   cudaSetDevice(c->device);
   for (DevBuf<double>* b : {&c->kxc, &c->kyc, &c->kxf, &c->kyf, &c->s_dev, &c->w_dev, &c->zero_s, &c->one_w, &c->a_dev})
     b->release();
-  for (DevBuf<double2>* b : {&c->twx, &c->twy, &c->bc, &c->inter, &c->slots, &c->Uc, &c->Ac, &c->Ac2, &c->full_tmp})
+  for (DevBuf<double2>* b : {&c->twx, &c->twy, &c->bc, &c->inter, &c->slots, &c->Uc, &c->Ac, &c->Ac2, &c->full_tmp,
+                             &c->bfull, &c->diag_cols})
     b->release();
+  c->diag_part.release();
   c->flags.release();
   if (c->flags_host) cudaFreeHost(c->flags_host);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -688,6 +712,8 @@ int pswe_set_topography(pswe_ctx* c, const double* b_dev, void* stream) {
   pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p);
   c->launches++;
   CU(cudaMemcpyAsync(c->bc.p, c->Uc.p, (size_t)c->Ky * c->Kx * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  TRY(c->bfull.alloc(c->full_elems()));
+  CU(cudaMemcpyAsync(c->bfull.p, b, c->full_elems() * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   c->version++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -938,6 +964,55 @@ done:
 double pswe_max_frequency(const pswe_ctx* c) { return c ? c->lam_max : 0.0; }
 
 int64_t pswe_launch_count(const pswe_ctx* c) { return c ? c->launches : 0; }
+
+int pswe_diagnostics(pswe_ctx* c, const double* u, const double* v, const double* e, double* out3, void* stream) {
+  if (!c || !u || !v || !e || !out3) return set_err(PSWE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaSetDevice(c->device));
+  if (!c->bfull.p) {  // flat bottom
+    TRY(c->bfull.alloc(c->full_elems()));
+    CU(cudaMemsetAsync(c->bfull.p, 0, c->full_elems() * sizeof(double2), st));
+  }
+  TRY(c->diag_cols.alloc((size_t)4 * (c->ny / 2 + 1) * c->nx));
+  TRY(c->diag_part.alloc((size_t)3 * c->nx));
+  const double2 *U = (const double2*)u, *V = (const double2*)v, *E = (const double2*)e;
+  int rc = PSWE_EUNSUPPORTED;
+  switch (c->nx) {
+    case 8: rc = launch_diag_cols<8>(c, U, V, E, c->bfull.p, st); break;
+    case 16: rc = launch_diag_cols<16>(c, U, V, E, c->bfull.p, st); break;
+    case 32: rc = launch_diag_cols<32>(c, U, V, E, c->bfull.p, st); break;
+    case 64: rc = launch_diag_cols<64>(c, U, V, E, c->bfull.p, st); break;
+    case 128: rc = launch_diag_cols<128>(c, U, V, E, c->bfull.p, st); break;
+    case 256: rc = launch_diag_cols<256>(c, U, V, E, c->bfull.p, st); break;
+    case 512: rc = launch_diag_cols<512>(c, U, V, E, c->bfull.p, st); break;
+  }
+  if (rc != PSWE_OK) return rc == PSWE_EUNSUPPORTED ? set_err(rc, "unsupported nx = %d", c->nx) : rc;
+  rc = PSWE_EUNSUPPORTED;
+  switch (c->ny) {
+    case 8: rc = launch_diag_rows<8>(c, st); break;
+    case 16: rc = launch_diag_rows<16>(c, st); break;
+    case 32: rc = launch_diag_rows<32>(c, st); break;
+    case 64: rc = launch_diag_rows<64>(c, st); break;
+    case 128: rc = launch_diag_rows<128>(c, st); break;
+    case 256: rc = launch_diag_rows<256>(c, st); break;
+    case 512: rc = launch_diag_rows<512>(c, st); break;
+  }
+  if (rc != PSWE_OK) return rc == PSWE_EUNSUPPORTED ? set_err(rc, "unsupported ny = %d", c->ny) : rc;
+  std::vector<double> part((size_t)3 * c->nx);
+  CU(cudaMemcpyAsync(part.data(), c->diag_part.p, part.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  double se = 0.0, sm = 0.0, vmax = 0.0;
+  for (int x = 0; x < c->nx; ++x) {  // rows in order: deterministic
+    se += part[3 * (size_t)x];
+    sm += part[3 * (size_t)x + 1];
+    vmax = std::max(vmax, part[3 * (size_t)x + 2]);
+  }
+  const double area = (c->Lx / c->nx) * (c->Ly / c->ny);  // cell_area = dx dy (grid.py:58-59)
+  out3[0] = se * area;
+  out3[1] = sm * area;
+  out3[2] = std::sqrt(vmax);
+  return PSWE_OK;
+}
 
 int pswe_profile_enable(pswe_ctx* c, int enable) {
   if (!c) return set_err(PSWE_EINVAL, "null context");
