@@ -386,6 +386,26 @@ def run_step_configs(pk, cases, torch, stream):
         out.append({"config": name, "grid": c.grid.nx, "M": c.M, "P": c.P, "steps": c.nsteps,
                     "run_ms": ms, "ms_per_step": ms / c.nsteps, "phase_dof_per_s": units / (ms * 1e-3),
                     "nonfinite": bool(bad[0])})
+    # fine-step reference solver (step_reference / cmd_reference, integrator.py:106-110,
+    # harness.py:92-99): T = 0, M = 0 (one node), dt = 180 s, 15 days = 7200 steps on C2's grid
+    c = cases.CASES["C2"]()
+    dt, nsteps = 180.0, 7200
+    cfg = pk.StepConfig(dt=dt, quadrature=pk.kernel_weights(0.0, 0), propagator_spec=pk.PropagatorSpec.exact())
+    ctx = pk.integrator._prepare(c.state, cfg, c.params)
+    U0 = pk.dynamics.upload(ctx, c.state)
+    U = [x.clone() for x in U0]
+    ctx.run(dt, 1, U)
+    torch.cuda.synchronize()
+    U = [x.clone() for x in U0]
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    bad = ctx.run(dt, nsteps, U)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    out.append({"config": "C2-fine-reference", "grid": c.grid.nx, "M": 0, "P": 1, "steps": nsteps, "dt": dt,
+                "run_ms": ms, "ms_per_step": ms / nsteps,
+                "phase_dof_per_s": 3 * nsteps * c.dof / (ms * 1e-3), "nonfinite": bool(bad[0])})
     return out
 
 

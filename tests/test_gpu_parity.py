@@ -109,6 +109,23 @@ def test_config_steps_match_reference(name):
         assert fin.t == float(z["t_final"])
 
 
+def test_fine_step_reference_matches_oracle():
+    """step_reference (integrator.py:106-110): T = 0, M = 0, dt = 180 s -- the
+    fine-step solver of cmd_reference, same kernels with one node."""
+    z = load_golden("C2")
+    grid, params, state, _ = golden_problem(z)
+    dt, n = 180.0, 20
+    one = pk.step_reference(state, dt, params)
+    cfg = pk.StepConfig(dt=dt, quadrature=pk.kernel_weights(0.0, 0), propagator_spec=pk.PropagatorSpec.exact())
+    traj = pk.run(state, cfg, params, t_end=n * dt)
+    S = O.Setup(grid.nx, grid.ny, grid.Lx, grid.Ly, params.f, params.g, params.H, params.b)
+    want1 = O.ssprk3_step(S, arr(state), dt, [0.0], [1.0])
+    wantn = O.run(S, arr(state), dt, n, [0.0], [1.0])
+    assert rel_l2(arr(one), want1) <= STEP_TOL
+    assert rel_l2(arr(traj.states[-1]), wantn) <= STEP_TOL
+    assert traj.states[-1].t == pytest.approx(n * dt)
+
+
 # ---------------------------------------------------------------- full sizes vs oracle
 def test_c5_512_rhs_matches_oracle():
     c = cases.case_c5(7, 8)  # 512^2, 15 phases
