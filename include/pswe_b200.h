@@ -137,6 +137,13 @@ int64_t pswe_launch_count(const pswe_ctx* ctx);
 int pswe_diagnostics(pswe_ctx* ctx, const double* u_dev, const double* v_dev, const double* eta_dev,
                      double* out3_host, void* stream);
 
+/* Physical fields (to_physical, grid.py:140-180, without its validation
+ * gate: real(ifft2(.)) via the Hermitian part) of u, v, eta into phys_dev =
+ * [3][nx][ny] doubles, row-major, y fastest -- the snapshot layout of
+ * io.py:37-70.  Asynchronous on the stream. */
+int pswe_to_physical(pswe_ctx* ctx, const double* u_dev, const double* v_dev, const double* eta_dev,
+                     double* phys_dev, void* stream);
+
 /* Tuning: bytes of chunk intermediates per lane (default 768 MiB, three lanes). */
 int pswe_set_chunk_bytes(pswe_ctx* ctx, size_t bytes);
 

@@ -55,6 +55,7 @@ SIGNATURES = {
     "pswe_max_frequency": (_d, [_vp]),
     "pswe_launch_count": (ctypes.c_int64, [_vp]),
     "pswe_diagnostics": (_i, [_vp, _vp, _vp, _vp, ctypes.POINTER(_d), _vp]),
+    "pswe_to_physical": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_set_chunk_bytes": (_i, [_vp, ctypes.c_size_t]),
     "pswe_profile_enable": (_i, [_vp, _i]),
     "pswe_profile_read": (_i, [_vp, ctypes.POINTER(_d), ctypes.POINTER(ctypes.c_int64), _i]),
@@ -347,6 +348,12 @@ class Context:
         out = (ctypes.c_double * 3)()
         _check(_lib.pswe_diagnostics(self.h, *(_dptr(x) for x in U), out, _stream(self.torch)))
         return float(out[0]), float(out[1]), float(out[2])
+
+    def to_physical(self, U):
+        """(3, nx, ny) float64 CUDA tensor of the physical u, v, eta."""
+        out = self.torch.empty((3, self.nx, self.ny), dtype=self.torch.float64, device=f"cuda:{self.device}")
+        _check(_lib.pswe_to_physical(self.h, *(_dptr(x) for x in U), _dptr(out), _stream(self.torch)))
+        return out
 
     def run(self, dt: float, nsteps: int, U):
         """In-place nsteps on U (list of 3 tensors). Returns (bad_step, stage, field)."""

@@ -67,9 +67,11 @@ __device__ __forceinline__ double2 diag_pair(const double2* D, int fa, int fb, i
   return cmk(A.x - B.y, A.y + B.x);
 }
 
+// part: [nx][3] row partials; phys (optional): [3][nx][ny] physical u, v, eta
 template <int NY>
 __global__ void __launch_bounds__(128) diag_rows_kernel(GridDev G, const double2* __restrict__ D, double H,
-                                                        double grav, double* __restrict__ part) {
+                                                        double grav, double* __restrict__ part,
+                                                        double* __restrict__ phys) {
   constexpr int T = WF<NY>::T, P = WF<NY>::P, GPW = WF<NY>::GPW;
   __shared__ double xbuf[4 * GPW * WF<NY>::XBUF];
   const int nx = G.nx;
@@ -87,6 +89,17 @@ __global__ void __launch_bounds__(128) diag_rows_kernel(GridDev G, const double2
 #pragma unroll
   for (int n1 = 0; n1 < P; ++n1) eb[n1] = diag_pair<NY>(D, 2, 3, t + T * n1, xr, nx);
   wfft_t1<NY, true>(eb, t, xb, wl);
+  if (phys != nullptr && active) {
+    const size_t nxy = (size_t)nx * NY;
+    double* pr = phys + (size_t)x * NY;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int y = t1_pos<NY>(t, i);
+      pr[y] = uv[i].x;
+      pr[nxy + y] = uv[i].y;
+      pr[2 * nxy + y] = eb[i].x;
+    }
+  }
   double se = 0.0, sm = 0.0, vmax = 0.0;
 #pragma unroll
   for (int i = 0; i < P; ++i) {

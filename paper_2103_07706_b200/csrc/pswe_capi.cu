@@ -317,10 +317,10 @@ int launch_diag_cols(pswe_ctx* c, const double2* u, const double2* v, const doub
   return PSWE_OK;
 }
 template <int NY>
-int launch_diag_rows(pswe_ctx* c, cudaStream_t st) {
+int launch_diag_rows(pswe_ctx* c, double* phys, cudaStream_t st) {
   const int per = 4 * WF<NY>::GPW;
   diag_rows_kernel<NY><<<(c->nx + per - 1) / per, 128, 0, st>>>(c->grid(), c->diag_cols.p, c->H, c->g,
-                                                                  c->diag_part.p);
+                                                                  c->diag_part.p, phys);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -965,9 +965,10 @@ double pswe_max_frequency(const pswe_ctx* c) { return c ? c->lam_max : 0.0; }
 
 int64_t pswe_launch_count(const pswe_ctx* c) { return c ? c->launches : 0; }
 
-int pswe_diagnostics(pswe_ctx* c, const double* u, const double* v, const double* e, double* out3, void* stream) {
-  if (!c || !u || !v || !e || !out3) return set_err(PSWE_EINVAL, "null argument");
-  cudaStream_t st = (cudaStream_t)stream;
+// full 2-D C2R of (u, v, eta, b) with row partials of the diagnostics; phys
+// (optional) receives the physical u, v, eta
+static int physical_fields(pswe_ctx* c, const double* u, const double* v, const double* e, double* phys,
+                           cudaStream_t st) {
   CU(cudaSetDevice(c->device));
   if (!c->bfull.p) {  // flat bottom
     TRY(c->bfull.alloc(c->full_elems()));
@@ -989,15 +990,31 @@ int pswe_diagnostics(pswe_ctx* c, const double* u, const double* v, const double
   if (rc != PSWE_OK) return rc == PSWE_EUNSUPPORTED ? set_err(rc, "unsupported nx = %d", c->nx) : rc;
   rc = PSWE_EUNSUPPORTED;
   switch (c->ny) {
-    case 8: rc = launch_diag_rows<8>(c, st); break;
-    case 16: rc = launch_diag_rows<16>(c, st); break;
-    case 32: rc = launch_diag_rows<32>(c, st); break;
-    case 64: rc = launch_diag_rows<64>(c, st); break;
-    case 128: rc = launch_diag_rows<128>(c, st); break;
-    case 256: rc = launch_diag_rows<256>(c, st); break;
-    case 512: rc = launch_diag_rows<512>(c, st); break;
+    case 8: rc = launch_diag_rows<8>(c, phys, st); break;
+    case 16: rc = launch_diag_rows<16>(c, phys, st); break;
+    case 32: rc = launch_diag_rows<32>(c, phys, st); break;
+    case 64: rc = launch_diag_rows<64>(c, phys, st); break;
+    case 128: rc = launch_diag_rows<128>(c, phys, st); break;
+    case 256: rc = launch_diag_rows<256>(c, phys, st); break;
+    case 512: rc = launch_diag_rows<512>(c, phys, st); break;
   }
   if (rc != PSWE_OK) return rc == PSWE_EUNSUPPORTED ? set_err(rc, "unsupported ny = %d", c->ny) : rc;
+  return PSWE_OK;
+}
+
+int pswe_to_physical(pswe_ctx* c, const double* u, const double* v, const double* e, double* phys,
+                                void* stream) {
+  if (!c || !u || !v || !e || !phys) return set_err(PSWE_EINVAL, "null argument");
+  CU(cudaSetDevice(c->device));
+  return physical_fields(c, u, v, e, phys, (cudaStream_t)stream);
+}
+
+int pswe_diagnostics(pswe_ctx* c, const double* u, const double* v, const double* e, double* out3,
+                                void* stream) {
+  if (!c || !u || !v || !e || !out3) return set_err(PSWE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaSetDevice(c->device));
+  TRY(physical_fields(c, u, v, e, nullptr, st));
   std::vector<double> part((size_t)3 * c->nx);
   CU(cudaMemcpyAsync(part.data(), c->diag_part.p, part.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
