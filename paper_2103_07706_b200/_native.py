@@ -119,7 +119,7 @@ def _stream(torch):
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-_PIN_OUT = {}
+_PIN = threading.local()  # per-thread pinned staging buffers (in / out)
 _POOL = None
 
 
@@ -137,10 +137,11 @@ def download_fields(tensors):
     torch = _torch()
     shape = tuple(tensors[0].shape)
     key = (shape, tensors[0].dtype, len(tensors))
-    pin = _PIN_OUT.get(key)
+    cache = _PIN.__dict__.setdefault("out", {})
+    pin = cache.get(key)
     if pin is None:
         pin = torch.empty((len(tensors),) + shape, dtype=tensors[0].dtype, pin_memory=True)
-        _PIN_OUT[key] = pin
+        cache[key] = pin
     for i, t in enumerate(tensors):
         pin[i].copy_(t, non_blocking=True)
     torch.cuda.current_stream().synchronize()
@@ -148,9 +149,6 @@ def download_fields(tensors):
     # fresh arrays fault their pages in on first write: copy the fields out in
     # parallel threads (numpy releases the GIL for the copy)
     return list(_copy_pool().map(lambda i: pn[i].copy(), range(len(tensors))))
-
-
-_PIN_IN = {}
 
 
 def upload_fields(arrays, device: int):
@@ -161,11 +159,12 @@ def upload_fields(arrays, device: int):
     arrays = [np.asarray(a) for a in arrays]
     shape = arrays[0].shape
     key = (shape, len(arrays), device)
-    ent = _PIN_IN.get(key)
+    cache = _PIN.__dict__.setdefault("in", {})
+    ent = cache.get(key)
     if ent is None:
         pin = torch.empty((len(arrays),) + shape, dtype=torch.complex128, pin_memory=True)
         ent = [pin, pin.numpy(), None]
-        _PIN_IN[key] = ent
+        cache[key] = ent
     pin, pn, ev = ent
     if ev is not None:
         ev.synchronize()
@@ -368,6 +367,14 @@ class Context:
 
 _ctx_cache: dict = {}
 _ctx_lock = threading.Lock()
+
+
+def release_thread_contexts() -> None:
+    """Drop the calling thread's cached contexts (frees their device scratch)."""
+    me = threading.get_ident()
+    with _ctx_lock:
+        for key in [k for k in _ctx_cache if k[-1] == me]:
+            del _ctx_cache[key]
 
 
 def context_for(nx, ny, Lx, Ly, f, g, H) -> Context:

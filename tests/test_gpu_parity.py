@@ -296,3 +296,21 @@ def test_graph_batched_run_matches_single_steps_bitwise():
         V, (st, fl) = ctx.ssprk3_step(c.dt, V)
         assert st == 0
     assert all(bool((a == b).all()) for a, b in zip(U, V))
+
+
+def test_window_sweep_matches_individual_runs_bitwise():
+    """8f item 2: all windows run concurrently (one context + stream each) and
+    each equals its own sequential run bitwise; errors vs a fine reference."""
+    c = cases.CASES["C2"]()
+    dt, t_end = c.dt, 2 * c.dt
+    windows = (0.0, 1800.0, 3600.0)
+    ref = pk.run(c.state, pk.StepConfig(dt=180.0, quadrature=pk.kernel_weights(0.0, 0),
+                                        propagator_spec=pk.PropagatorSpec.exact()), c.params, t_end).states[-1]
+    res = pk.window_sweep(c.state, c.params, dt, t_end, windows, M=8, reference=ref)
+    assert [r.T for r in res] == list(windows)
+    for r in res:
+        cfg = pk.make_step_config(c.grid, c.params, dt=dt, T=r.T, M=8 if r.T > 0 else 0)
+        solo = pk.run(c.state, cfg, c.params, t_end).states[-1]
+        assert np.array_equal(arr(r.final), arr(solo))
+        assert r.final.t == solo.t
+        assert np.isfinite(r.l2_eta) and np.isfinite(r.l2_u)
