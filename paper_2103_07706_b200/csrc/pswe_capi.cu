@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -49,12 +50,19 @@ int set_err(int code, const char* fmt, ...) {
 
 bool pow2_ok(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
 
+// Contexts may be driven from several host threads (window sweep).  A CUDA
+// graph capture on one thread must not overlap another thread's
+// device-synchronising calls (cudaFree, context setup), so captures and
+// those calls are serialised process-wide.
+std::recursive_mutex g_capture_mutex;
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   int alloc(size_t count) {
     if (count <= n) return PSWE_OK;
+    std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
@@ -63,6 +71,7 @@ struct DevBuf {
     return PSWE_OK;
   }
   void release() {
+    std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
@@ -544,6 +553,7 @@ int ensure_step_graph(pswe_ctx* c, double dt, Full3 Ain, Full3w Bout, size_t byt
   c->prof = false;
   const int64_t l0 = c->launches;
   CU(cudaStreamSynchronize(st));
+  std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
   CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
   int rc = step_impl(c, dt, Ain, Bout, st);
   cudaError_t ce = cudaMemcpyAsync((void*)Ain.u, Bout.u, bytes3, cudaMemcpyDeviceToDevice, st);
@@ -578,6 +588,7 @@ const char* pswe_last_error(void) { return g_err.c_str(); }
 
 int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, double g, double H, int device) {
   if (!out) return set_err(PSWE_EINVAL, "null context pointer");
+  std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);  // setup synchronises the device
   *out = nullptr;
   if (nx < 8 || nx % 2 != 0) return set_err(PSWE_EINVAL, "nx must be even and >= 8, got %d", nx);
   if (ny < 8 || ny % 2 != 0) return set_err(PSWE_EINVAL, "ny must be even and >= 8, got %d", ny);
@@ -679,6 +690,7 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
 
 void pswe_destroy(pswe_ctx* c) {
   if (!c) return;
+  std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
   cudaSetDevice(c->device);
   for (DevBuf<double>* b : {&c->kxc, &c->kyc, &c->kxf, &c->kyf, &c->s_dev, &c->w_dev, &c->zero_s, &c->one_w, &c->a_dev})
     b->release();

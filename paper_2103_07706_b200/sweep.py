@@ -5,8 +5,9 @@ The reference runs one full trajectory per window T in sequence
 ``_check_window_sweep``) and compares each final state with a fine-step
 reference run.  Here every window is an independent device-resident run
 (its own native context: quadrature, phase table, intermediates) on its own
-CUDA stream, all launched together from host threads, so the windows share
-the GPU: small windows (few phases) fill the gaps of large ones.  The
+CUDA stream, all launched together from persistent host threads, so the
+windows share the GPU: small windows (few phases) fill the gaps of large
+ones.  The
 per-window results are bitwise identical to running the windows one by one.
 """
 
@@ -21,6 +22,30 @@ from . import _native
 from .integrator import make_step_config, run
 
 __all__ = ["WindowResult", "window_sweep", "l2_error_normalized"]
+
+# Persistent worker threads: a native context is cached per (grid, physics,
+# thread), so keeping the workers alive keeps each window's context (phase
+# table, intermediates, captured step graph) warm across sweeps.
+_POOL = None
+_POOL_SIZE = 0
+_TLS = threading.local()
+
+
+def _pool(n):
+    global _POOL, _POOL_SIZE
+    if _POOL is None or _POOL_SIZE < n:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=n, thread_name_prefix="pswe-window")
+        _POOL_SIZE = n
+    return _POOL
+
+
+def _worker_stream(torch):
+    s = getattr(_TLS, "stream", None)
+    if s is None:
+        s = torch.cuda.Stream()
+        _TLS.stream = s
+    return s
 
 
 @dataclass
@@ -56,31 +81,17 @@ def window_sweep(initial, params, dt: float, t_end: float, windows, M=None, prop
     for T in windows:
         m = None if M is None else (M if T > 0 else 0)
         cfgs.append(make_step_config(grid, params, dt=dt, T=float(T), M=m, propagator=propagator))
-    results = [None] * len(cfgs)
-    errors = [None] * len(cfgs)
     device = torch.cuda.current_device()
 
     def work(i):
-        try:
-            torch.cuda.set_device(device)
-            stream = torch.cuda.Stream()
-            with torch.cuda.stream(stream):  # each window on its own stream (and context)
-                traj = run(initial, cfgs[i], params, t_end, snapshot_every=snapshot_every)
-            stream.synchronize()
-            results[i] = traj
-        except BaseException as exc:  # re-raised on the calling thread
-            errors[i] = exc
-        finally:
-            _native.release_thread_contexts()  # the per-thread contexts die with the window
+        torch.cuda.set_device(device)
+        stream = _worker_stream(torch)
+        with torch.cuda.stream(stream):  # each window on its own stream (and context)
+            traj = run(initial, cfgs[i], params, t_end, snapshot_every=snapshot_every)
+        stream.synchronize()
+        return traj
 
-    threads = [threading.Thread(target=work, args=(i,), name=f"pswe-window-{i}") for i in range(len(cfgs))]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    for e in errors:
-        if e is not None:
-            raise e
+    results = list(_pool(len(cfgs)).map(work, range(len(cfgs))))
     out = []
     for T, cfg, traj in zip(windows, cfgs, results):
         r = WindowResult(T=float(T), M=int(cfg.quadrature.M), final=traj.states[-1], trajectory=traj)
