@@ -224,16 +224,41 @@ def workload_config(case):
             "l2": "flushed (256 MiB write) before every timed step"}
 
 
-def load_traffic(n):
-    """ncu dram bytes per passB launch from the committed profile summary, if present."""
+def load_traffic(n, kernel, phases_per_launch):
+    """ncu DRAM bytes (read + write) per launch of `kernel`, scaled from the
+    committed per-phase figure of the latest profile summary, if present."""
     for path in sorted((ROOT / "profiles").glob("ncu_summary_r*.json"), reverse=True):
         try:
             d = json.loads(path.read_text())
-            ent = d.get("passB", {}).get(str(n))
-            if ent:
-                return ent
+            ent = d.get(kernel, {}).get(str(n))
+            if isinstance(ent, dict) and "bytes_per_phase" in ent:
+                return ent["bytes_per_phase"] * phases_per_launch
         except (OSError, ValueError):
             continue
+    return None
+
+
+def fp64_roofline(n, P, ms_per_step, sm_clock_ghz=1.965):
+    """The fp64 side of the bound: the evaluation's DP thread-instruction count
+    (per-phase ncu counts of the committed profile summary x P) against the
+    B200's 64 fp64 lanes per SM per clock (148 SMs), and its flop rate against
+    the 2 x 64 x 148 x clock peak.  None when no summary for this n exists."""
+    for path in sorted((ROOT / "profiles").glob("ncu_summary_r*.json"), reverse=True):
+        try:
+            d = json.loads(path.read_text())
+        except (OSError, ValueError):
+            continue
+        ents = [d.get(k, {}).get(str(n)) for k in ("passA", "passB", "passC")]
+        if not all(isinstance(e, dict) and "dp_thread_instr_per_phase" in e for e in ents):
+            continue
+        instr = P * sum(e["dp_thread_instr_per_phase"] for e in ents)
+        flop = P * sum(e["dp_flop_per_phase"] for e in ents)
+        lanes_per_s = 64 * 148 * sm_clock_ghz * 1e9
+        floor_ms = 1e3 * instr / lanes_per_s
+        return {"bound": "fp64", "dp_thread_instr": instr, "floor_ms": floor_ms,
+                "pipe_frac": floor_ms / ms_per_step, "flop": flop,
+                "achieved_tflops": flop / (ms_per_step * 1e-3) / 1e12,
+                "peak_tflops": 2 * lanes_per_s / 1e12, "source": path.name}
     return None
 
 
@@ -286,7 +311,12 @@ def run_ours(args, ws, rank, local):
     units = ws * P * case.dof * args.steps
     value = units / (dev_ms * 1e-3)
 
-    # ---- per-kernel split (CUDA events around each launch, separate pass)
+    # ---- per-kernel split (CUDA events around each launch, separate pass).
+    # One chunk lane here: with overlapping lanes an event pair would also
+    # time the other lanes' kernels; serialised, the shares are comparable
+    # with the ncu launch list.
+    lanes = ctx.lanes
+    ctx.set_lanes(1)
     ctx.profile(True)
     for _ in range(args.steps):
         flush_l2(flush)
@@ -294,6 +324,7 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     prof = ctx.profile_read()
     ctx.profile(False)
+    ctx.set_lanes(lanes)
     ab = alg_bytes(n, P)
     peak = peak_hbm()
     kern = {}
@@ -309,11 +340,12 @@ def run_ours(args, ws, rank, local):
     phases_per_launch = P / max(kern[dom]["launches_per_step"], 1e-9)
     dom_bytes = ab[f"{dom}_phase"] * phases_per_launch if dom.startswith("pass") else 3 * 16 * n * n
     achieved = dom_bytes / (per_launch_ms * 1e-3) / 1e9
-    traffic = load_traffic(n)
+    traffic = load_traffic(n, dom, phases_per_launch)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak["value"],
                 "unit": "GB/s", "frac": achieved / peak["value"], "peak_source": peak["source"],
                 "traffic": traffic, "alg_bytes_per_launch": dom_bytes,
                 "launch_ms": per_launch_ms}
+    fp64 = fp64_roofline(n, P, ms_per_step)
     rhs_achieved = ab["B_eval"] / (ms_per_step * 1e-3) / 1e9
     rhs_roofline = {"bound": "hbm", "B_eval": ab["B_eval"], "achieved": rhs_achieved,
                     "peak": peak["value"], "unit": "GB/s", "frac": rhs_achieved / peak["value"],
@@ -354,7 +386,7 @@ def run_ours(args, ws, rank, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded planar C5 stand-in, SURVEY.md 8d)",
             "config": workload_config(case) | {"parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
-            "roofline": roofline, "rhs_roofline": rhs_roofline, "kernels": kern,
+            "roofline": roofline, "rhs_roofline": rhs_roofline, "fp64": fp64, "kernels": kern,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "gpu": torch.cuda.get_device_name(local), "sweep": sweep, "step_configs": steps_info,
         }

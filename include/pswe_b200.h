@@ -147,6 +147,10 @@ int pswe_to_physical(pswe_ctx* ctx, const double* u_dev, const double* v_dev, co
 /* Tuning: bytes of chunk intermediates per lane (default 768 MiB, three lanes). */
 int pswe_set_chunk_bytes(pswe_ctx* ctx, size_t bytes);
 
+/* Tuning: chunk lanes (streams whose chunks overlap), 1..4, default 3. */
+int pswe_set_lanes(pswe_ctx* ctx, int lanes);
+int pswe_get_lanes(const pswe_ctx* ctx);
+
 /* Per-kernel CUDA-event timing (instrumentation for bench.py).  While
  * enabled, every RHS kernel launch is bracketed by events on its stream.
  * Kernel classes: 0 pass A, 1 pass B, 2 pass C, 3 slot reduction, 4 pack,

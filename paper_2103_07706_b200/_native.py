@@ -57,6 +57,8 @@ SIGNATURES = {
     "pswe_diagnostics": (_i, [_vp, _vp, _vp, _vp, ctypes.POINTER(_d), _vp]),
     "pswe_to_physical": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_set_chunk_bytes": (_i, [_vp, ctypes.c_size_t]),
+    "pswe_set_lanes": (_i, [_vp, _i]),
+    "pswe_get_lanes": (_i, [_vp]),
     "pswe_profile_enable": (_i, [_vp, _i]),
     "pswe_profile_read": (_i, [_vp, ctypes.POINTER(_d), ctypes.POINTER(ctypes.c_int64), _i]),
 }
@@ -239,6 +241,13 @@ class Context:
 
     def set_chunk_bytes(self, nbytes: int) -> None:
         _check(_lib.pswe_set_chunk_bytes(self.h, int(nbytes)))
+
+    @property
+    def lanes(self) -> int:
+        return int(_lib.pswe_get_lanes(self.h))
+
+    def set_lanes(self, lanes: int) -> None:
+        _check(_lib.pswe_set_lanes(self.h, int(lanes)))
 
     def set_quadrature(self, s: np.ndarray, w: np.ndarray) -> None:
         s = np.ascontiguousarray(s, dtype=np.float64)

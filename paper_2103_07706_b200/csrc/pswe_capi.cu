@@ -1077,4 +1077,15 @@ int pswe_set_chunk_bytes(pswe_ctx* c, size_t bytes) {
   return PSWE_OK;
 }
 
+int pswe_set_lanes(pswe_ctx* c, int lanes) {
+  if (!c) return set_err(PSWE_EINVAL, "null context");
+  if (lanes < 1 || lanes > pswe_ctx::MAX_LANES)
+    return set_err(PSWE_EINVAL, "lanes must be in [1, %d], got %d", pswe_ctx::MAX_LANES, lanes);
+  c->n_lanes = lanes;
+  c->version++;
+  return PSWE_OK;
+}
+
+int pswe_get_lanes(const pswe_ctx* c) { return c ? c->n_lanes : 0; }
+
 }  // extern "C"
