@@ -221,9 +221,27 @@ int launchB_t(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO
 }
 
 template <int NY>
+int launchB_pair(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, cudaStream_t st) {
+  using W = PassBW<NY>;
+  const size_t smem = W::template bytes<true>();
+  auto kern = passB_pair_kernel<NY>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int ntp = ((np + 1) / 2) * c->nx;
+  const int blocks = (ntp + W::GPC - 1) / W::GPC;
+  ProfScope ps(c, 1, st);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, mI1, mO);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+template <int NY>
 int launchB(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2, cudaStream_t st) {
   if constexpr (NY >= 64) {
-    if (passB_fast(c)) return launchB_t<NY, true>(c, np, mI1, mO, I2, st);
+    if (passB_fast(c)) {
+      if (!getenv("PSWE_NO_PAIR")) return launchB_pair<NY>(c, np, mI1, mO, st);
+      return launchB_t<NY, true>(c, np, mI1, mO, I2, st);
+    }
   }
   return launchB_t<NY, false>(c, np, mI1, mO, I2, st);
 }
