@@ -206,15 +206,15 @@ int passB_rows(int ny) { return 4 * 32 / std::max(1, ny / 16); }
 // tensor-memory stash + TMA tile store path: NY >= 64 and whole tiles per phase
 bool passB_fast(const pswe_ctx* c) { return c->ny >= 64 && c->nx % passB_rows(c->ny) == 0; }
 
-template <int NY, bool FAST>
-int launchB_t(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2, cudaStream_t st) {
+template <int NY>
+int launchB_small(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cudaStream_t st) {
   using W = PassBW<NY>;
-  const size_t smem = W::template bytes<FAST>();
-  auto kern = passB_kernel<NY, FAST>;
+  const size_t smem = W::template bytes<false>();
+  auto kern = passB_kernel<NY>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, mI1, mO, I2);
+  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, mI1, I2);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -238,12 +238,9 @@ int launchB_pair(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap&
 template <int NY>
 int launchB(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2, cudaStream_t st) {
   if constexpr (NY >= 64) {
-    if (passB_fast(c)) {
-      if (!getenv("PSWE_NO_PAIR")) return launchB_pair<NY>(c, np, mI1, mO, st);
-      return launchB_t<NY, true>(c, np, mI1, mO, I2, st);
-    }
+    if (passB_fast(c)) return launchB_pair<NY>(c, np, mI1, mO, st);
   }
-  return launchB_t<NY, false>(c, np, mI1, mO, I2, st);
+  return launchB_small<NY>(c, np, mI1, I2, st);
 }
 
 template <int NX>
@@ -356,8 +353,8 @@ int launch_diag_rows(pswe_ctx* c, double* phys, cudaStream_t st) {
 // TMA tensor map of a rank-4 fp64 tensor (dims innermost first, byte strides
 // of dims 1..3) with box `box`; the encoder comes from the driver through the
 // runtime's entry-point query, so the library links only against cudart.
-int encode_map(CUtensorMap* m, void* base, const cuuint64_t dims[4], const cuuint64_t strides[3],
-               const cuuint32_t box[4]) {
+int encode_map(CUtensorMap* m, void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+               const cuuint32_t* box, int rank = 4, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -366,8 +363,8 @@ int encode_map(CUtensorMap* m, void* base, const cuuint64_t dims[4], const cuuin
       return set_err(PSWE_ECUDA, "cuTensorMapEncodeTiled not available from the driver");
   }
   const cuuint32_t es[4] = {1, 1, 1, 1};
-  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(PSWE_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
   return PSWE_OK;
@@ -383,13 +380,19 @@ int map_rows_I1(const pswe_ctx* c, double2* I1, int CP, CUtensorMap* m) {
 }
 
 // I2[p][f][j][x] written by pass-B tiles: box (re/im, R x, Ky j, 2 fields)
+// I2[p][f][j][x] written by pass-B tiles: rank 3 in doubles (2 nx, Ky, 4 CP),
+// box (2R doubles = the tile's R rows, Ky, 2 fields).  The staging tile is
+// swizzled (64-byte rows for R = 4, 128-byte rows for R = 8) so that the
+// warps' column writes into it are bank-conflict free.
 int map_tiles_I2(const pswe_ctx* c, double2* I2, int CP, CUtensorMap* m) {
   const cuuint64_t nx = c->nx, Ky = c->Ky;
-  const cuuint64_t dims[4] = {2, nx, Ky, (cuuint64_t)4 * CP};
-  const cuuint64_t strides[3] = {16, nx * 16, Ky * nx * 16};
   const cuuint32_t R = (cuuint32_t)std::min<cuuint64_t>(passB_rows(c->ny), nx);
-  const cuuint32_t box[4] = {2, R, (cuuint32_t)Ky, 2};
-  return encode_map(m, I2, dims, strides, box);
+  const cuuint64_t dims[3] = {2 * nx, Ky, (cuuint64_t)4 * CP};
+  const cuuint64_t strides[2] = {nx * 16, Ky * nx * 16};
+  const cuuint32_t box[3] = {2 * R, (cuuint32_t)Ky, 2};
+  const CUtensorMapSwizzle swz = R == 4 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                 : (R == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+  return encode_map(m, I2, dims, strides, box, 3, swz);
 }
 
 // Averaged RHS on compact data: chunks of phases through passes A, B, C,

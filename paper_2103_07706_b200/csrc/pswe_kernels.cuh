@@ -256,7 +256,7 @@ struct PassBW {
   }
   template <bool FAST>
   __host__ __device__ static constexpr size_t stage_bytes() {
-    return FAST ? ((size_t)2 * Ky * R * sizeof(double2) + 127) / 128 * 128 : 0;
+    return FAST ? ((size_t)2 * Ky * R * sizeof(double2) + 127) / 128 * 128 + 1024 : 0;
   }
   template <bool FAST>
   static size_t bytes() {
@@ -394,15 +394,17 @@ __device__ __forceinline__ void uv_get4(double2 (&q)[4], const double2* uv, uint
   }
 }
 
-template <int NY, bool FAST>
+// Small grids (NY < 64 or tiles that do not divide nx): one row per task
+// group, the (u, v) stash in shared memory, outputs stored directly into the
+// column-major I2.  The FAST path is passB_pair_kernel.
+template <int NY>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
-    passB_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mO,
-                 double2* __restrict__ I2) {
+    passB_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, double2* __restrict__ I2) {
   using W = PassBW<NY>;
-  constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA, R = W::R;
+  constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA;
   extern __shared__ __align__(128) unsigned char sbytes[];
   constexpr int Ky = W::Ky;  // == Gd.Ky
-  constexpr size_t WB = W::template warp_bytes<FAST>();
+  constexpr size_t WB = W::template warp_bytes<false>();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane % T, g = lane / T;
   unsigned char* wbase = sbytes + (size_t)warp * WB;
@@ -410,19 +412,16 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   double* xb = reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) + (size_t)g * WF<NY>::XBUF;
   double2* uv = reinterpret_cast<double2*>(reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) +
                                            (size_t)GPW * WF<NY>::XBUF) +
-                (size_t)g * P * T;  // [P][T] (small-grid path only)
+                (size_t)g * P * T;  // [P][T]
   uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + WB - 8);
-  double2* stage = reinterpret_cast<double2*>(sbytes + (size_t)W::WARPS * WB);  // [2][Ky][R] (FAST)
-  double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * WB + W::template stage_bytes<FAST>());
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(kys + Ky);
+  double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * WB);
   const int ntask = np * Gd.nx;
   const int first_task = (blockIdx.x * W::WARPS + warp) * GPW;
   const int task = first_task + g;
   const bool active = task < ntask;
   const int pl = active ? task / Gd.nx : 0, x = active ? task % Gd.nx : 0;
   const size_t KyNX = (size_t)Ky * Gd.nx;
-  double2* out = I2 + (size_t)pl * 4 * KyNX + x;  // I2[pl][f][j][x] (small-grid path)
-  const int rc = warp * GPW + g;                  // row within the CTA tile
+  double2* out = I2 + (size_t)pl * 4 * KyNX + x;  // I2[pl][f][j][x]
   const double2* mypre = pre + (size_t)g * 2 * KYA;
   for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
 
@@ -430,16 +429,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  if constexpr (FAST) {
-    if (warp == 0) tmem_alloc(tslot, 128);
-    tmem_fence_before_sync();
-  }
   __syncthreads();
-  uint32_t taddr = 0;
-  if constexpr (FAST) {
-    tmem_fence_after_sync();
-    taddr = *tslot + ((uint32_t)(32 * warp) << 16);  // this warp's lane quadrant
-  }
   passB_prefetch<NY>(0, lane, pre, bar, &mI, first_task, ntask, Gd.nx);
 
   double2 v[P];
@@ -454,82 +444,72 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     if (it < 3) passB_prefetch<NY>(it + 1, lane, pre, bar, &mI, first_task, ntask, Gd.nx);
     wfft_t1<NY, true, true>(v, t, xb, wl);
     if (it == 0) {
-      if constexpr (FAST) {
-        tmem_stash16(taddr, v);
-        tmem_wait_st();
-      } else {
 #pragma unroll
-        for (int i = 0; i < P; ++i) uv[i * T + t] = v[i];
-      }
+      for (int i = 0; i < P; ++i) uv[i * T + t] = v[i];
     } else if (it == 1) {
 #pragma unroll
-      for (int i0 = 0; i0 < P; i0 += 4) {
-        double2 q[4];
-        uv_get4<NY, FAST>(q, uv, taddr, i0, t);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          pa[i0 + k] = -(q[k].x * v[i0 + k].x + q[k].y * v[i0 + k].y);  // A = -(u ux + v uy)
-      }
-      if constexpr (FAST) {  // park A in tensor memory across the next transform
-        tmem_stash16d(taddr + 64, pa);
-        tmem_wait_st();
+      for (int i = 0; i < P; ++i) {
+        const double2 q = uv[i * T + t];
+        pa[i] = -(q.x * v[i].x + q.y * v[i].y);  // A = -(u ux + v uy)
       }
     } else if (it == 2) {
 #pragma unroll
-      for (int i0 = 0; i0 < P; i0 += 4) {
-        double2 q[4];
-        uv_get4<NY, FAST>(q, uv, taddr, i0, t);
-        double a4[4];
-        if constexpr (FAST) {
-          uint32_t r[8];
-          tmem_ld_x8(taddr + 64 + 2 * i0, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 4; ++k) a4[k] = __hiloint2double(r[2 * k + 1], r[2 * k]);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) a4[k] = pa[i0 + k];
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)  // A + iB, B = -(u vx + v vy)
-          v[i0 + k] = cmk(a4[k], -(q[k].x * v[i0 + k].x + q[k].y * v[i0 + k].y));
+      for (int i = 0; i < P; ++i) {
+        const double2 q = uv[i * T + t];
+        v[i] = cmk(pa[i], -(q.x * v[i].x + q.y * v[i].y));  // A + iB, B = -(u vx + v vy)
       }
     } else {
 #pragma unroll
-      for (int i0 = 0; i0 < P; i0 += 4) {
-        double2 q[4];
-        uv_get4<NY, FAST>(q, uv, taddr, i0, t);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)  // C + iD = u depth + i v depth
-          v[i0 + k] = cmk(q[k].x * v[i0 + k].x, q[k].y * v[i0 + k].x);
+      for (int i = 0; i < P; ++i) {
+        const double2 q = uv[i * T + t];
+        v[i] = cmk(q.x * v[i].x, q.y * v[i].x);  // C + iD = u depth + i v depth
       }
     }
     if (it < 2) continue;
     wfft_t2<NY, false>(v, t, xb, wl);
     const int fo = it == 2 ? 0 : 2;
-    if constexpr (FAST) {
-      // the previous tile store has finished reading the staging tile
-      if (threadIdx.x == 0) bulk_wait_read0();
-      __syncthreads();
-      unpack_store<NY>(v, t, stage + rc, stage + (size_t)Ky * R + rc, Ky, R, true);
-      fence_proxy_async();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int t0 = blockIdx.x * R;  // first row of the tile (one phase)
-        tma_store_4d(&mO, 0, t0 % Gd.nx, 0, 4 * (t0 / Gd.nx) + fo, stage);
-        bulk_commit();
-      }
-    } else {
-      unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
-    }
+    unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
   }
-  if constexpr (FAST) {
-    if (threadIdx.x == 0) bulk_wait0();
-    tmem_fence_before_sync();
-    __syncthreads();
-    if (warp == 0) {
-      tmem_fence_after_sync();
-      tmem_dealloc(*tslot, 128);
+}
+
+// Unpack a forward pair transform (as unpack_store) into the CTA's staging
+// tile [2 fields][Ky][R] at tile row rc, in the swizzled layout of the TMA
+// store map: a tile line (one field, one j: R complex = R * 16 bytes) has its
+// 16-byte chunks permuted, chunk' = chunk ^ ((line >> 1) & 3) for 64-byte
+// lines (R = 4, SWIZZLE_64B) and chunk ^ (line & 7) for 128-byte lines
+// (R = 8, SWIZZLE_128B), so the warp's writes (consecutive j) hit distinct
+// banks.  Wider tiles are unswizzled.
+template <int NY, int R>
+__device__ __forceinline__ int stage_slot(int line, int rc) {
+  if constexpr (R == 4)
+    return line * 4 + (rc ^ ((line >> 1) & 3));
+  else if constexpr (R == 8)
+    return line * 8 + (rc ^ (line & 7));
+  else
+    return line * R + rc;
+}
+
+template <int NY, int R>
+__device__ __forceinline__ void unpack_stage(const double2* v, int t, double2* stage, int rc) {
+  constexpr int T = WF<NY>::T, P = WF<NY>::P, Ky = NY / 3 + 1;
+  constexpr int MU = (Ky + T - 1) / T;
+#pragma unroll
+  for (int m = 0; m < MU; ++m) {
+    const int j = t + T * m;
+    double2 zm;
+    if constexpr (T == 1) {
+      zm = v[(P - m) & (P - 1)];
+    } else {
+      const double2 src = v[P - 1 - m];
+      double2 r;
+      r.x = __shfl_sync(0xffffffffu, src.x, (T - t) & (T - 1), T);
+      r.y = __shfl_sync(0xffffffffu, src.y, (T - t) & (T - 1), T);
+      zm = t == 0 ? v[(P - m) & (P - 1)] : r;
+    }
+    if (j < Ky) {
+      const double2 a = v[m];
+      stage[stage_slot<NY, R>(j, rc)] = cmk(0.5 * (a.x + zm.x), 0.5 * (a.y - zm.y));
+      stage[stage_slot<NY, R>(Ky + j, rc)] = cmk(0.5 * (a.y + zm.y), -0.5 * (a.x - zm.x));
     }
   }
 }
@@ -578,7 +558,9 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   double2* preb = pre + KYA;
   double* xb = reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) + (size_t)g * WF<NY>::XBUF;
   uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + WB - 8);
-  double2* stage = reinterpret_cast<double2*>(sbytes + (size_t)W::WARPS * WB);  // [2][Ky][R]
+  // [2][Ky][R] swizzled staging tile, 1024-byte aligned (swizzle atom)
+  const uint32_t stage_pad = (1024u - (smem_u32(sbytes + (size_t)W::WARPS * WB) & 1023u)) & 1023u;
+  double2* stage = reinterpret_cast<double2*>(sbytes + (size_t)W::WARPS * WB + stage_pad);
   double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * WB + W::template stage_bytes<true>());
   uint32_t* tslot = reinterpret_cast<uint32_t*>(kys + Ky);
   const int nx = Gd.nx;
@@ -697,11 +679,11 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
       const int fo = it == 2 ? 0 : 2;
       if (threadIdx.x == 0) bulk_wait_read0();
       __syncthreads();
-      unpack_store<NY>(v, t, stage + rc, stage + (size_t)Ky * R + rc, Ky, R, true);
+      unpack_stage<NY, R>(v, t, stage, rc);
       fence_proxy_async();
       __syncthreads();
       if (threadIdx.x == 0) {
-        tma_store_4d(&mO, 0, x0, 0, 4 * (p0 + sub) + fo, stage);
+        tma_store_3d(&mO, 2 * x0, 0, 4 * (p0 + sub) + fo, stage);
         bulk_commit();
       }
     }
