@@ -314,3 +314,22 @@ def test_window_sweep_matches_individual_runs_bitwise():
         assert np.array_equal(arr(r.final), arr(solo))
         assert r.final.t == solo.t
         assert np.isfinite(r.l2_eta) and np.isfinite(r.l2_u)
+
+
+def test_chebyshev_route_step_and_run_match_oracle():
+    """The Chebyshev exponential route (propagator.py:161-191) through the
+    whole stepper: 3 averaged RHS + 5 stage exponentials per step, vs the
+    oracle with the same Lambda / n_poly, over a 3-step run on C2's problem."""
+    z = load_golden("C2")
+    grid, params, state, _ = golden_problem(z)
+    cfg = pk.make_step_config(grid, params, dt=float(z["dt"]), T=float(z["T_half"]), M=8,
+                              propagator="chebyshev")
+    spec = cfg.propagator_spec
+    S = O.Setup(grid.nx, grid.ny, grid.Lx, grid.Ly, params.f, params.g, params.H, params.b)
+    prop = O.Propagator("chebyshev", spec.Lambda, spec.n_poly)
+    q = cfg.quadrature
+    want = O.run(S, arr(state), cfg.dt, 3, q.s, q.w, prop)
+    got = pk.run(state, cfg, params, t_end=3 * cfg.dt).states[-1]
+    err = rel_l2(arr(got), want)
+    print(f"chebyshev 3-step run rel L2 vs oracle {err:.3e}")
+    assert err <= STEP_TOL
