@@ -144,10 +144,10 @@ int pswe_diagnostics(pswe_ctx* ctx, const double* u_dev, const double* v_dev, co
 int pswe_to_physical(pswe_ctx* ctx, const double* u_dev, const double* v_dev, const double* eta_dev,
                      double* phys_dev, void* stream);
 
-/* Tuning: bytes of chunk intermediates per lane (default 768 MiB, three lanes). */
+/* Tuning: bytes of chunk intermediates per lane (default 1536 MiB, four lanes). */
 int pswe_set_chunk_bytes(pswe_ctx* ctx, size_t bytes);
 
-/* Tuning: chunk lanes (streams whose chunks overlap), 1..4, default 3. */
+/* Tuning: chunk lanes (streams whose chunks overlap), 1..4, default 4. */
 int pswe_set_lanes(pswe_ctx* ctx, int lanes);
 int pswe_get_lanes(const pswe_ctx* ctx);
 

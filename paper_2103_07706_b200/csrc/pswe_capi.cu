@@ -103,12 +103,12 @@ struct pswe_ctx {
   double Lambda = 0;
   DevBuf<double> a_dev;
   // scratch
-  size_t chunk_bytes = size_t(768) << 20;
+  size_t chunk_bytes = size_t(1536) << 20;
   DevBuf<double2> inter, slots, Uc, Ac, Ac2;
   static constexpr int MAX_LANES = 4;
   cudaStream_t st_lane[MAX_LANES - 1] = {};  // chunk lanes 1.. (lane 0 is the caller's stream)
   cudaEvent_t ev_lane[MAX_LANES - 1] = {};
-  int n_lanes = 3;
+  int n_lanes = 4;
   // cached CUDA graph of one SSPRK3 step (pswe_run)
   cudaGraphExec_t step_exec = nullptr;
   double graph_dt = 0.0;
@@ -415,17 +415,21 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     c->ctab_cur = tb.p;
   }
   const size_t per_phase = (size_t)9 * c->Ky * c->nx;  // I1 (5 fields) + I2 (4 fields), double2
-  int CP = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
-  CP = std::min(CP, P);
-  const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
-  // Two chunk "lanes" on two streams when there is more than one chunk: the
-  // next chunk's passes fill the previous chunk's launch tails.  Each lane
-  // has its own intermediates and slot set; chunks alternate lanes, every
-  // slot accumulates its lane's chunks in order and the final reduction sums
-  // lane 0's slots then lane 1's -- a fixed order, so results stay bitwise
-  // deterministic.
-  const int nchunks = (P + CP - 1) / CP;
+  // Chunk "lanes" on separate streams when there is more than one chunk:
+  // the chunks' passes overlap and fill each other's launch tails.  Each lane
+  // has its own intermediates and slot set; chunks go round-robin over the
+  // lanes, every slot accumulates its lane's chunks in order and the final
+  // reduction sums lane 0's slots, then lane 1's, ... -- a fixed order, so
+  // results stay bitwise deterministic.  The phases are split into a
+  // multiple of `lanes` equal chunks no larger than chunk_bytes, so the lanes
+  // finish together.
+  const int cpmax = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
+  int nchunks = (P + cpmax - 1) / cpmax;
   const int lanes = std::max(1, std::min(c->n_lanes, nchunks));
+  nchunks = (nchunks + lanes - 1) / lanes * lanes;
+  const int CP = std::max(1, std::min(P, (P + nchunks - 1) / nchunks));
+  nchunks = (P + CP - 1) / CP;
+  const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
   TRY(c->inter.alloc(per_phase * CP * lanes));
   TRY(c->slots.alloc((size_t)lanes * Gc * c->compact_elems()));
   if (getenv("PSWE_DEBUG_POISON")) {  // debug: NaN-fill intermediates to expose unwritten entries

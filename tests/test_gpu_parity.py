@@ -183,7 +183,7 @@ def test_chunking_does_not_change_results():
         ctx.set_chunk_bytes(1)  # one phase per chunk
         one = ctx.averaged_tendency_compact(Uc).cpu().numpy()
     finally:
-        ctx.set_chunk_bytes(768 << 20)
+        ctx.set_chunk_bytes(1536 << 20)
     assert rel_l2(one, base) <= 1e-14
 
 
