@@ -12,6 +12,7 @@ import ctypes
 import os
 import pathlib
 import threading
+import weakref
 
 import numpy as np
 
@@ -121,7 +122,7 @@ def _stream(torch):
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-_PIN = threading.local()  # per-thread pinned staging buffers (in / out)
+_PIN = threading.local()  # per-thread pinned staging buffers for uploads
 _POOL = None
 
 
@@ -133,24 +134,64 @@ def _copy_pool():
     return _POOL
 
 
+class _PinnedPool:
+    """Pinned host buffers handed out as the numpy arrays a call returns.
+
+    A buffer goes back to the pool when its array is garbage-collected
+    (weakref.finalize), so a caller that drops results between calls gets
+    them without a fresh cudaHostAlloc and without a host copy; results that
+    are kept simply keep their buffer."""
+
+    def __init__(self):
+        self.free = {}
+        self.lock = threading.Lock()
+
+    def take(self, shape, dtype):
+        key = (tuple(shape), dtype)
+        with self.lock:
+            lst = self.free.get(key)
+            if lst:
+                return lst.pop()
+        return _torch().empty(shape, dtype=dtype, pin_memory=True)
+
+    def give(self, key, tensor):
+        with self.lock:
+            self.free.setdefault(key, []).append(tensor)
+
+    def array(self, tensor):
+        # The holder owns the buffer for numpy: every view of the returned
+        # array keeps the holder (not the array) as its base, so the buffer is
+        # recycled only when no view of it is left.
+        holder = _PinnedHolder(tensor)
+        weakref.finalize(holder, self.give, (tuple(tensor.shape), tensor.dtype), tensor)
+        return np.asarray(holder)
+
+
+class _PinnedHolder:
+    """numpy array-interface exporter of one pinned tensor's memory."""
+
+    _TYPESTR = {"torch.complex128": "<c16", "torch.float64": "<f8"}
+
+    def __init__(self, tensor):
+        self.t = tensor
+        self.__array_interface__ = {"shape": tuple(tensor.shape), "typestr": self._TYPESTR[str(tensor.dtype)],
+                                    "data": (tensor.data_ptr(), False), "version": 3}
+
+
+_POOL_OUT = _PinnedPool()
+
+
 def download_fields(tensors):
-    """CUDA tensors -> fresh numpy arrays: D2H into a reused pinned staging
-    buffer (one stream sync), then a host copy out of it."""
+    """CUDA tensors -> numpy arrays backed by pooled pinned host memory (one
+    stream sync, no host copy)."""
     torch = _torch()
-    shape = tuple(tensors[0].shape)
-    key = (shape, tensors[0].dtype, len(tensors))
-    cache = _PIN.__dict__.setdefault("out", {})
-    pin = cache.get(key)
-    if pin is None:
-        pin = torch.empty((len(tensors),) + shape, dtype=tensors[0].dtype, pin_memory=True)
-        cache[key] = pin
-    for i, t in enumerate(tensors):
-        pin[i].copy_(t, non_blocking=True)
+    hosts = []
+    for t in tensors:
+        h = _POOL_OUT.take(t.shape, t.dtype)
+        h.copy_(t, non_blocking=True)
+        hosts.append(h)
     torch.cuda.current_stream().synchronize()
-    pn = pin.numpy()
-    # fresh arrays fault their pages in on first write: copy the fields out in
-    # parallel threads (numpy releases the GIL for the copy)
-    return list(_copy_pool().map(lambda i: pn[i].copy(), range(len(tensors))))
+    return [_POOL_OUT.array(h) for h in hosts]
 
 
 def upload_fields(arrays, device: int):

@@ -1,0 +1,30 @@
+"""Where the end-to-end averaged_tendency call spends its time (512^2, M=256)."""
+import sys, time
+sys.path.insert(0, ".")
+import numpy as np, torch
+import paper_2103_07706_b200 as pk
+from paper_2103_07706_b200 import cases, dynamics, propagator
+
+c = cases.case_c5(7, 256)
+spec = pk.PropagatorSpec.exact()
+for _ in range(2):
+    pk.averaged_tendency(c.state, c.quadrature, c.params, spec)
+torch.cuda.synchronize()
+T = {}
+def mark(k, t0):
+    torch.cuda.synchronize(); T[k] = T.get(k, 0) + time.perf_counter() - t0
+n = 5
+for _ in range(n):
+    t0 = time.perf_counter(); ctx = dynamics.context(c.state, c.params); propagator.configure(ctx, spec)
+    ctx.set_quadrature(c.quadrature.s, c.quadrature.w); mark("setup", t0)
+    t0 = time.perf_counter(); U = dynamics.upload(ctx, c.state); mark("upload", t0)
+    t0 = time.perf_counter(); out = ctx.averaged_tendency(U); mark("compute", t0)
+    t0 = time.perf_counter(); res = dynamics.download(out); mark("download", t0)
+    t0 = time.perf_counter(); st = dynamics.rebuild(c.state, res, c.state.t); mark("rebuild", t0)
+    del res, st, out, U
+t0 = time.perf_counter()
+for _ in range(n):
+    r = pk.averaged_tendency(c.state, c.quadrature, c.params, spec)
+torch.cuda.synchronize()
+tot = (time.perf_counter() - t0) / n
+print({k: round(1e3 * v / n, 3) for k, v in T.items()}, "full call", round(1e3 * tot, 3))
