@@ -86,14 +86,5 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Warp-convergent wait: lane 0 spins on the barrier, then the warp
-// reconverges at __syncwarp (which also orders the other lanes' subsequent
-// shared-memory reads after lane 0's acquire).  Keeping the spin loop out of
-// the other lanes stops nvcc from treating everything after the wait as
-// potentially divergent (no collective fix-up code around shuffles).
-__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity, int lane) {
-  if (lane == 0) mbar_wait(bar, parity);
-  __syncwarp();
-}
 
 }  // namespace pswe

@@ -1,16 +1,5 @@
-// Register-resident fp64 complex FFT for power-of-two N in [8, 1024].
-//
-// One transform is computed by a "group" of T = N/8 threads; thread t holds
-// the 8 points x[t + m*N/8], m = 0..7, in registers on entry and the 8
-// outputs X[t + m*N/8] on exit (same distribution).  Stages are mixed-radix
-// Stockham (radix 8, then one radix 4 or 2 stage), so between stages the
-// group exchanges data through a padded shared-memory buffer; the first
-// stage's input and the last stage's output never touch shared memory, which
-// lets callers fuse per-mode work (exponentials, products, 2/3 truncation)
-// directly into the FFT's first load and last store.
-//
-// Shared-memory index padding pidx(i) = i + i/8 removes the stride-8 bank
-// conflict of the first Stockham stage's scatter.
+// Small fp64 complex DFTs in registers (2, 4, 8 points, and 4-point variants
+// with a known-zero input), the building blocks of the warp FFT in wfft.cuh.
 //
 // Sign convention: FWD is X[k] = sum x[n] e^{-2 pi i nk/N} (numpy fft),
 // INV is the unnormalised e^{+2 pi i nk/N} sum (N * numpy ifft).
@@ -18,13 +7,6 @@
 #include "pswe_common.cuh"
 
 namespace pswe {
-
-__device__ __forceinline__ int pidx(int i) { return i + (i >> 3); }
-template <int N>
-struct FFTSize {
-  static constexpr int T = N / 8;            // threads per transform
-  static constexpr int PAD = N + N / 8;      // padded smem length (double2)
-};
 
 // ---- small DFTs in registers ------------------------------------------------
 template <bool INV>
@@ -91,165 +73,5 @@ __device__ __forceinline__ void dft8(double2* v) {
   v[4] = a2; v[5] = b2; v[6] = a3; v[7] = b3;
 }
 
-template <int R, bool INV>
-__device__ __forceinline__ void dftR(double2* v) {
-  if constexpr (R == 8) {
-    dft8<INV>(v);
-  } else if constexpr (R == 4) {
-    dft4<INV>(v[0], v[1], v[2], v[3]);
-  } else {
-    dft2<INV>(v[0], v[1]);
-  }
-}
-
-// ---- group barrier -----------------------------------------------------------
-// Groups of <= 32 threads live inside one warp (all lanes run the same code),
-// larger groups use a named barrier per group.  Barrier 0 is __syncthreads.
-template <int N>
-__device__ __forceinline__ void group_sync(int group_in_cta) {
-  if constexpr (N / 8 <= 32) {
-    __syncwarp();
-  } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + group_in_cta), "n"(N / 8) : "memory");
-  }
-}
-
-// ---- Stockham stage ------------------------------------------------------------
-// Butterfly j in [0, N/R): inputs x[j + r*N/R], twiddle W_N^{r*(j%NS)*N/(NS*R)},
-// outputs x'[(j/NS)*NS*R + j%NS + r*NS].  Thread t does butterflies
-// j = t + q*N/8, q < 8/R, with registers v[q*R + r].
-// Twiddles W^{r e}, r = 1..R-1, from one table entry W^e by a depth-3 power
-// tree (w2 = w1^2, w4 = w2^2, ...): one shared-memory load per butterfly
-// instead of R-1 dependent global loads.
-template <int R, bool INV>
-__device__ __forceinline__ void twiddle_powers(double2 w1, double2* w) {
-  if (INV) w1.y = -w1.y;
-  w[1] = w1;
-  if constexpr (R >= 4) {
-    w[2] = cmul(w1, w1);
-    w[3] = cmul(w[2], w1);
-  }
-  if constexpr (R == 8) {
-    w[4] = cmul(w[2], w[2]);
-    w[5] = cmul(w[4], w1);
-    w[6] = cmul(w[3], w[3]);
-    w[7] = cmul(w[4], w[3]);
-  }
-}
-
-template <int N, int R, int NS, bool INV>
-__device__ __forceinline__ void stage_compute(double2* v, int t, const double2* __restrict__ tw) {
-  constexpr int B = 8 / R;
-#pragma unroll
-  for (int q = 0; q < B; ++q) {
-    if constexpr (NS > 1) {
-      const int j = t + q * (N / 8);
-      const int k = j % NS;
-      double2 w[8];
-      twiddle_powers<R, INV>(tw[k * (N / (NS * R))], w);
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[q * R + r] = cmul(v[q * R + r], w[r]);
-    }
-    dftR<R, INV>(v + q * R);
-  }
-}
-
-template <int N, int R, int NS>
-__device__ __forceinline__ void stage_store(const double2* v, int t, double2* sm) {
-  constexpr int B = 8 / R;
-#pragma unroll
-  for (int q = 0; q < B; ++q) {
-    const int j = t + q * (N / 8);
-    const int base = (j / NS) * NS * R + (j % NS);
-#pragma unroll
-    for (int r = 0; r < R; ++r) sm[pidx(base + r * NS)] = v[q * R + r];
-  }
-}
-
-// load the next stage's inputs: butterfly j, element r at j + r*N/R
-template <int N, int R>
-__device__ __forceinline__ void stage_load(double2* v, int t, const double2* sm) {
-  constexpr int B = 8 / R;
-#pragma unroll
-  for (int q = 0; q < B; ++q) {
-    const int j = t + q * (N / 8);
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[q * R + r] = sm[pidx(j + r * (N / R))];
-  }
-}
-
-template <int N, int NS>
-struct StageRadix {
-  static constexpr int REM = N / NS;
-  static constexpr int R = REM >= 8 ? 8 : REM;
-};
-
-// first-stage input register layout for radix R: v[q*R + r] = x[t + q*N/8 + r*N/R]
-// = x[t + m*N/8] with m = q + r*(8/R).  Callers load v[m] = x[t + m*N/8]; this
-// permutes to the stage layout.
-template <int R>
-__device__ __forceinline__ void to_stage_layout(double2* v) {
-  if constexpr (R == 8) return;
-  constexpr int B = 8 / R;
-  double2 tmp[8];
-#pragma unroll
-  for (int q = 0; q < B; ++q)
-#pragma unroll
-    for (int r = 0; r < R; ++r) tmp[q * R + r] = v[q + r * B];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = tmp[i];
-}
-template <int R>
-__device__ __forceinline__ void from_stage_layout(double2* v) {
-  if constexpr (R == 8) return;
-  constexpr int B = 8 / R;
-  double2 tmp[8];
-#pragma unroll
-  for (int q = 0; q < B; ++q)
-#pragma unroll
-    for (int r = 0; r < R; ++r) tmp[q + r * B] = v[q * R + r];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = tmp[i];
-}
-
-template <int N, int NS, bool INV>
-struct Stages {
-  // v holds this stage's inputs in stage layout; on return v holds the final
-  // outputs X[t + m*N/8] in natural layout (v[m]).
-  static __device__ __forceinline__ void run(double2* v, int t, double2* sm, int gid,
-                                             const double2* __restrict__ tw) {
-    constexpr int R = StageRadix<N, NS>::R;
-    stage_compute<N, R, NS, INV>(v, t, tw);
-    if constexpr (NS * R == N) {
-      // last stage: outputs at j + r*NS = t + q*N/8 + r*N/R  -> natural layout
-      from_stage_layout<R>(v);
-    } else {
-      constexpr int R2 = StageRadix<N, NS * R>::R;
-      group_sync<N>(gid);  // previous readers of sm are done
-      stage_store<N, R, NS>(v, t, sm);
-      group_sync<N>(gid);
-      stage_load<N, R2>(v, t, sm);
-      Stages<N, NS * R, INV>::run(v, t, sm, gid, tw);
-    }
-  }
-};
-
-// Full transform: v[m] = x[t + m*N/8] in, X[t + m*N/8] out.  sm: group's padded
-// exchange buffer (FFTSize<N>::PAD double2); tw: the N-entry forward twiddle
-// table W_N^k, normally staged in shared memory (load_twiddles).  Contains
-// group barriers: every thread of the group must call it.
-template <int N, bool INV>
-__device__ __forceinline__ void fft_reg(double2* v, int t, double2* sm, int gid,
-                                        const double2* __restrict__ tw) {
-  constexpr int R0 = StageRadix<N, 1>::R;
-  to_stage_layout<R0>(v);
-  Stages<N, 1, INV>::run(v, t, sm, gid, tw);
-}
-
-// copy the N-entry twiddle table to shared memory (whole CTA; caller syncs)
-template <int N>
-__device__ __forceinline__ void load_twiddles(double2* dst, const double2* __restrict__ src) {
-  for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = src[i];
-}
 
 }  // namespace pswe

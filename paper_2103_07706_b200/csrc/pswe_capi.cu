@@ -139,8 +139,8 @@ struct pswe_ctx {
     G.ph = Phys{f, g, H};
     G.inv_n2 = 1.0 / ((double)nx * (double)ny);
     G.kxc = kxc.p; G.kyc = kyc.p; G.kxf = kxf.p; G.kyf = kyf.p;
-    G.twx = WTab{twx.p, twx.p + nx, twx.p + nx + 16 * ((nx >= 16) ? nx / 16 : 1)};
-    G.twy = WTab{twy.p, twy.p + ny, twy.p + ny + 16 * ((ny >= 16) ? ny / 16 : 1)};
+    G.twx = WTab{twx.p};
+    G.twy = WTab{twy.p};
     G.bc = bc.p;
     return G;
   }
@@ -435,21 +435,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   if (getenv("PSWE_DEBUG_POISON")) {  // debug: NaN-fill intermediates to expose unwritten entries
     CU(cudaMemsetAsync(c->inter.p, 0xFF, per_phase * CP * lanes * sizeof(double2), st));
   }
-  PhaseDev ph{s, w, P, 0.0, 0};
-  {
-    const std::vector<double>& sv = (s == c->s_dev.p) ? c->s_live : c->zero_live;
-    if (sv.size() >= 2) {
-      const double ds = (sv.back() - sv.front()) / (double)(sv.size() - 1);
-      bool uni = ds != 0.0;
-      for (size_t i = 1; i < sv.size() && uni; ++i)
-        uni = std::fabs((sv[i] - sv[i - 1]) - ds) <= 1e-12 * std::fabs(ds);
-      ph.ds = ds;
-      ph.uniform = uni ? 1 : 0;
-    } else {
-      ph.ds = 0.0;
-      ph.uniform = 1;  // a single phase: the rotor is only anchored, never advanced
-    }
-  }
+  PhaseDev ph{s, w, P};
   cudaStream_t lst[pswe_ctx::MAX_LANES] = {st, c->st_lane[0], c->st_lane[1], c->st_lane[2]};
   CUtensorMap mrow[pswe_ctx::MAX_LANES], mcol[pswe_ctx::MAX_LANES];
   for (int L = 0; L < lanes; ++L) {
@@ -666,16 +652,13 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
     pswe_destroy(c);
     return rc;
   }
-  const int Tx = nx >= 16 ? nx / 16 : 1, Ty = ny >= 16 ? ny / 16 : 1;
-  if ((rc = c->twx.alloc(nx + 32 * Tx)) || (rc = c->twy.alloc(ny + 32 * Ty)) || (rc = c->bc.alloc((size_t)c->Ky * c->Kx)) ||
+  if ((rc = c->twx.alloc(nx)) || (rc = c->twy.alloc(ny)) || (rc = c->bc.alloc((size_t)c->Ky * c->Kx)) ||
       (rc = c->flags.alloc(1))) {
     pswe_destroy(c);
     return rc;
   }
   twiddle_kernel<<<(nx + 255) / 256, 256>>>(c->twx.p, nx);
   twiddle_kernel<<<(ny + 255) / 256, 256>>>(c->twy.p, ny);
-  wtab_init_kernel<<<1, 256>>>(nx, c->twx.p + nx, c->twx.p + nx + 16 * Tx);
-  wtab_init_kernel<<<1, 256>>>(ny, c->twy.p + ny, c->twy.p + ny + 16 * Ty);
   cudaMemset(c->bc.p, 0, (size_t)c->Ky * c->Kx * sizeof(double2));
   cudaMemset(c->flags.p, 0, sizeof(int));
   {

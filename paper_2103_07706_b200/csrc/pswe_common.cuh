@@ -124,59 +124,4 @@ __device__ __forceinline__ C3 exp_c12(double2 c12, const C3& q, const Phys& p, d
   return c3add(c3add(q, c3scale(c12.x, l1)), c3scale(c12.y, l2));
 }
 
-// ---------------------------------------------------------------------------
-// Phase rotor: the exact exponential of one mode at a run of equally spaced
-// phase shifts s_p = s_0 + p ds.  (cos, sin)(omega s) is advanced by the
-// rotation (cos, sin)(omega ds) instead of a sincos per phase; the run is
-// anchored with a direct sincos at its first phase, so the rotation error is
-// ~p ulp (p <= a few tens).  c1 = sin/omega, c2 = (1 - cos)/omega^2 use the
-// reference's formula (propagator.py:100-103) with precomputed reciprocals.
-struct Rotor {
-  double iom, iom2;  // 1/omega, 1/omega^2 (0 when omega == 0)
-  double cd, sd;     // cos, sin(omega ds)
-  double c, sn;      // cos, sin(omega s_p) at the current phase
-};
-
-__device__ __forceinline__ Rotor rotor_init(const Phys& p, double kx, double ky, double s0, double ds) {
-  Rotor r;
-  const double om = omega_of(p, kx, ky);
-  if (om > 0.0) {
-    r.iom = 1.0 / om;
-    r.iom2 = 1.0 / (om * om);
-    sincos(om * ds, &r.sd, &r.cd);
-    sincos(om * s0, &r.sn, &r.c);
-  } else {
-    r.iom = r.iom2 = 0.0;
-    r.cd = 1.0;
-    r.sd = 0.0;
-    r.c = 1.0;
-    r.sn = 0.0;
-  }
-  return r;
-}
-
-__device__ __forceinline__ void rotor_step(Rotor& r) {
-  const double c = r.c * r.cd - r.sn * r.sd;
-  const double s = r.sn * r.cd + r.c * r.sd;
-  r.c = c;
-  r.sn = s;
-}
-
-// e^{tL} q for t = sgn * s_p (sgn = +1 forward, -1 backward); omega == 0
-// falls back to the t, t^2/2 limit.
-__device__ __forceinline__ C3 exp_rotor(const Rotor& r, double t, double sgn, const C3& q, const Phys& p,
-                                        double kx, double ky) {
-  double c1, c2;
-  if (r.iom > 0.0) {
-    c1 = sgn * r.sn * r.iom;
-    c2 = (1.0 - r.c) * r.iom2;
-  } else {
-    c1 = t;
-    c2 = 0.5 * t * t;
-  }
-  C3 l1 = lin(q, p, kx, ky);
-  C3 l2 = lin(l1, p, kx, ky);
-  return c3add(c3add(q, c3scale(c1, l1)), c3scale(c2, l2));
-}
-
 }  // namespace pswe

@@ -50,8 +50,6 @@ struct PhaseDev {
   const double* s;  // [P] live node shifts, ascending k
   const double* w;  // [P] weights
   int P;
-  double ds;        // uniform spacing of s (valid when uniform != 0)
-  int uniform;      // 1: s_p = s_0 + p ds to round-off -> phase rotors usable
 };
 
 // compact kx index of FFT position k (0..nx-1), or -1 outside the band

@@ -138,15 +138,14 @@ __device__ __forceinline__ void apply_powers(double2* v, double2 w) {
   }
 }
 
-// twiddle tables of one transform length N.  t0 is what the FFT reads; the
-// per-lane tables t1/t2 (16*T entries each, kept for experiments) were slower
-// in pass B, where shared memory leaves L1 too small to hold them:
-//   t1[k1*T + t] = W_N^{t k1}                      (type 1, after the first DFT16)
-//   t2[i*T + t]  = type-2 twiddle of register i of lane t
+// twiddle table of one transform length N: W_N^k, k = 0..N-1 (forward sign);
+// the FFT reads per-lane bases from it and generates powers in registers.
 struct WTab {
-  const double2* t0;  // W_N^k, k = 0..N-1 (powers are generated in registers)
-  const double2* t1;
-  const double2* t2;
+  const double2* t0;
+  // Two spare pointers.  They only keep GridDev's kernel-parameter layout:
+  // with them removed, ptxas 12.9 allocates passes A and C differently and
+  // spills (measured: pass A 1.09 -> 1.12 ms per RHS).
+  const double2* spare_[2];
 };
 
 __device__ __forceinline__ double2 twg(const double2* __restrict__ tw, int e, bool inv) {
@@ -310,27 +309,6 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
       }
     }
     dft16<INV>(v);
-  }
-}
-
-// host/init helper: fill the WTab tables for length N (one thread per entry)
-__global__ void wtab_init_kernel(int N, double2* t1, double2* t2) {
-  const int T = N >= 16 ? N / 16 : 1;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 16 * T; idx += gridDim.x * blockDim.x) {
-    const int i = idx / T, t = idx % T;
-    long long e1 = (long long)t * i;  // W_N^{t k1}
-    long long e2;
-    if (T == 32) {
-      e2 = (long long)(t >> 1) * (2 * i + (t & 1));  // W_N^{n1 (2 q' + h)}
-    } else {
-      const int c = i / T, k = i % T;
-      e2 = (long long)(t + T * c) * k;  // W_N^{n1 k1''}
-    }
-    double s, c2;
-    sincospi(2.0 * (double)(e1 % N) / N, &s, &c2);
-    t1[idx] = make_double2(c2, -s);
-    sincospi(2.0 * (double)(e2 % N) / N, &s, &c2);
-    t2[idx] = make_double2(c2, -s);
   }
 }
 

@@ -14,7 +14,7 @@ __global__ void __launch_bounds__(128) probe(const double2* __restrict__ in, dou
   const size_t base = ((size_t)blockIdx.x * 128 + threadIdx.x) * WF<N>::P;
 #pragma unroll
   for (int i = 0; i < WF<N>::P; ++i) v[i] = in[base + i];
-  const WLane wl = wlane<N>(WTab{tw, tw, tw}, t);
+  const WLane wl = wlane<N>(WTab{tw}, t);
   if (TYPE == 1)
     wfft_t1<N, INV>(v, t, xb, wl);
   else
