@@ -172,19 +172,30 @@ def test_repeated_evaluations_are_bitwise_identical(level, M):
         assert np.array_equal(ctx.averaged_tendency_compact(Uc).cpu().numpy(), first)
 
 
-def test_chunking_does_not_change_results():
-    c = cases.case_c5(5, 32)  # 128^2, 63 phases
+@pytest.mark.parametrize("level", [5, 7])
+def test_chunking_and_lanes_do_not_change_results(level):
+    """Chunk size and lane count only regroup the phase sum (and the pass-B
+    phase pairing): results agree to round-off, and each configuration is
+    itself bitwise reproducible."""
+    c = cases.case_c5(level, 32)  # 63 phases
     ctx = pk.dynamics.context(c.state, c.params)
     ctx.set_propagator("exact")
     ctx.set_quadrature(c.quadrature.s, c.quadrature.w)
     Uc = ctx.pack(pk.dynamics.upload(ctx, c.state))
     base = ctx.averaged_tendency_compact(Uc).cpu().numpy()
+    lanes0 = ctx.lanes
+    per_phase = 9 * 16 * (c.grid.ny // 3 + 1) * c.grid.nx
     try:
-        ctx.set_chunk_bytes(1)  # one phase per chunk
-        one = ctx.averaged_tendency_compact(Uc).cpu().numpy()
+        for chunk, lanes in ((1, 1), (1, 4), (7 * per_phase, 2), (16 * per_phase, 3), (1536 << 20, 1)):
+            ctx.set_chunk_bytes(chunk)
+            ctx.set_lanes(lanes)
+            a = ctx.averaged_tendency_compact(Uc).cpu().numpy()
+            b = ctx.averaged_tendency_compact(Uc).cpu().numpy()
+            assert np.array_equal(a, b), (chunk, lanes)
+            assert rel_l2(a, base) <= 1e-14, (chunk, lanes)
     finally:
         ctx.set_chunk_bytes(1536 << 20)
-    assert rel_l2(one, base) <= 1e-14
+        ctx.set_lanes(lanes0)
 
 
 def test_rectangular_grid_matches_oracle():
