@@ -244,9 +244,12 @@ __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WLa
           recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
           recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
           const double2 e0 = h ? recv : v[c];
-          const double2 e1 = h ? v[8 + c] : recv;
-          const double2 w = h ? w32(8 + c, INV) : w32(c, INV);  // W_32^{k2'}
-          const double2 we1 = cmul(w, e1);
+          // W_32^{8+c} = W_32^c W_32^8 and W_32^8 = +-i: the odd lane's operand
+          // is rotated (a register swap + sign) and the twiddle is the
+          // lane-uniform constant W_32^c
+          const double2 o = v[8 + c];
+          const double2 e1 = h ? (INV ? cmk(-o.y, o.x) : cmk(o.y, -o.x)) : recv;
+          const double2 we1 = cmul(w32(c, INV), e1);
           v[c] = cadd(e0, we1);
           v[8 + c] = csub(e0, we1);
         }
