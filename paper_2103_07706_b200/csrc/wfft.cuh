@@ -288,13 +288,15 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
         for (int cc = 0; cc < 8; ++cc) {
           const double2 a = v[cc], b = v[8 + cc];
           const double2 sv = cadd(a, b);
-          const double2 dv = cmul(csub(a, b), h ? w32(8 + cc, INV) : w32(cc, INV));
+          // W_32^{8+cc} = W_32^cc (+-i): lane-uniform twiddle, the odd lane's
+          // copy rotated by a register swap + sign
+          const double2 dv = cmul(csub(a, b), w32(cc, INV));
           const double2 send = h ? sv : dv;
           double2 recv;
           recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
           recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
           q[cc] = h ? recv : sv;
-          q[8 + cc] = h ? dv : recv;
+          q[8 + cc] = h ? (INV ? cmk(-dv.y, dv.x) : cmk(dv.y, -dv.x)) : recv;
         }
         dft16<INV>(q);  // Z[n1][2 q' + h]
         // twiddle W_N^{n1 (2q'+h)} = W^{n1 h} (W^{2 n1})^{q'}
