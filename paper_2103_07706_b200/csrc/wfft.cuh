@@ -282,6 +282,7 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
             for (int n1 = 0; n1 < 16; ++n1) v[n1].y = xb[n1 * S + t])
       } else {
         const int h = t & 1, n1 = t >> 1;
+        const double2 wn1 = wsel(wl.wn1, INV);  // W_N^{n1}
         // s_c = a + b, d_c = (a - b) W_32^c for this lane's c = 8h + cc
         double2 q[16];
 #pragma unroll
@@ -289,8 +290,11 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
           const double2 a = v[cc], b = v[8 + cc];
           const double2 sv = cadd(a, b);
           // W_32^{8+cc} = W_32^cc (+-i): lane-uniform twiddle, the odd lane's
-          // copy rotated by a register swap + sign
-          const double2 dv = cmul(csub(a, b), w32(cc, INV));
+          // copy rotated by a register swap + sign.  dv only ever feeds the
+          // odd lane's DFT16 (sent by the even lane, kept by the odd one), so
+          // the odd lane's output factor W_N^{n1} is applied here, to both
+          // lanes alike, instead of as a lane-divergent multiply afterwards.
+          const double2 dv = cmul(cmul(csub(a, b), w32(cc, INV)), wn1);
           const double2 send = h ? sv : dv;
           double2 recv;
           recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
@@ -298,13 +302,8 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
           q[cc] = h ? recv : sv;
           q[8 + cc] = h ? (INV ? cmk(-dv.y, dv.x) : cmk(dv.y, -dv.x)) : recv;
         }
-        dft16<INV>(q);  // Z[n1][2 q' + h]
+        dft16<INV>(q);  // Z[n1][2 q' + h] (the odd lane's already times W^{n1})
         // twiddle W_N^{n1 (2q'+h)} = W^{n1 h} (W^{2 n1})^{q'}
-        if (h) {
-          const double2 b1 = wsel(wl.wn1, INV);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) q[k] = cmul(q[k], b1);
-        }
         apply_powers<16>(q, wsel(wl.w2n1, INV));
         PSWE_XPOSE(
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].x,
