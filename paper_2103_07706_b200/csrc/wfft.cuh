@@ -154,25 +154,21 @@ __device__ __forceinline__ double2 twg(const double2* __restrict__ tw, int e, bo
   return w;
 }
 
-// Per-lane twiddle bases (forward sign), loaded once per kernel instead of
-// once per transform: W_N^t (type 1 and type 2 for T <= 16), W_N^{n1} and
-// W_N^{2 n1} with n1 = t/2 (type 2, T == 32).
+// Per-lane twiddle bases (forward sign) read on use from the (L1-resident)
+// table rather than held in registers for the whole kernel: W_N^t (type 1,
+// and type 2 for T <= 16), W_N^{n1} and W_N^{2 n1} with n1 = t/2 (type 2,
+// T == 32).
 struct WLane {
-  double2 wt, wn1, w2n1;
+  const double2* tw;
+  int t;
+  __device__ __forceinline__ double2 wt() const { return __ldg(tw + t); }
+  __device__ __forceinline__ double2 wn1() const { return __ldg(tw + (t >> 1)); }
+  __device__ __forceinline__ double2 w2n1() const { return __ldg(tw + 2 * (t >> 1)); }
 };
 
 template <int N>
 __device__ __forceinline__ WLane wlane(const WTab tw, int t) {
-  WLane w;
-  if constexpr (N >= 32) {
-    w.wt = __ldg(tw.t0 + t);
-    w.wn1 = __ldg(tw.t0 + (t >> 1));
-    w.w2n1 = __ldg(tw.t0 + ((2 * (t >> 1)) & (N - 1)));
-  } else {
-    w.wt = w.wn1 = w.w2n1 = cmk(1.0, 0.0);
-    if constexpr (N >= 16) w.wt = __ldg(tw.t0 + t);
-  }
-  return w;
+  return WLane{tw.t0, t};
 }
 
 __device__ __forceinline__ double2 wsel(double2 w, bool inv) { return inv ? cmk(w.x, -w.y) : w; }
@@ -219,7 +215,7 @@ __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WLa
     constexpr int T = WF<N>::T, S = WF<N>::S;
     dft16<INV, BAND && (N >= 64)>(v);
     if constexpr (T > 1) {
-      apply_powers<16>(v, wsel(wl.wt, INV));  // W_N^{t k1}
+      apply_powers<16>(v, wsel(wl.wt(), INV));  // W_N^{t k1}
       if constexpr (T <= 16) {
         constexpr int C = 16 / T;
         PSWE_XPOSE(
@@ -273,7 +269,7 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
         for (int c = 0; c < C; ++c) {
           dftL<T, INV>(v + c * T);  // Z[n1][k1''], k1'' = 0..T-1
           // W_N^{n1 k1''}, n1 = t + T c: base W_N^t W_16^c (N = 16 T)
-          apply_powers<T>(v + c * T, cmul(wsel(wl.wt, INV), w16(c, INV)));
+          apply_powers<T>(v + c * T, cmul(wsel(wl.wt(), INV), w16(c, INV)));
         }
         PSWE_XPOSE(
             for (int c = 0; c < C; ++c) _Pragma("unroll") for (int k = 0; k < T; ++k) xb[(t + T * c) * S + k] = v[c * T + k].x,
@@ -282,7 +278,7 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
             for (int n1 = 0; n1 < 16; ++n1) v[n1].y = xb[n1 * S + t])
       } else {
         const int h = t & 1, n1 = t >> 1;
-        const double2 wn1 = wsel(wl.wn1, INV);  // W_N^{n1}
+        const double2 wn1 = wsel(wl.wn1(), INV);  // W_N^{n1}
         // s_c = a + b, d_c = (a - b) W_32^c for this lane's c = 8h + cc
         double2 q[16];
 #pragma unroll
@@ -304,7 +300,7 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
         }
         dft16<INV>(q);  // Z[n1][2 q' + h] (the odd lane's already times W^{n1})
         // twiddle W_N^{n1 (2q'+h)} = W^{n1 h} (W^{2 n1})^{q'}
-        apply_powers<16>(q, wsel(wl.w2n1, INV));
+        apply_powers<16>(q, wsel(wl.w2n1(), INV));
         PSWE_XPOSE(
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].x,
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].y,
