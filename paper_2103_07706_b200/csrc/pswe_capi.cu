@@ -249,7 +249,14 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
   // of the 3 x 148 resident CTAs, each CTA keeping >= 4 phases to amortise its
   // prologue and slot update.  Pick the Gc with the best wave efficiency.
   const int cols = (c->Ky + PassCW<NX>::GPW - 1) / PassCW<NX>::GPW;
-  const int slots = 3 * 148;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, passC_kernel<NX>, PassCW<NX>::WARPS * 32,
+                                                    PassCW<NX>::bytes(c->Kx)) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 3;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int slots = per_sm * sms;
   int best = 1;
   double best_eff = 0.0;
   for (int g = 1; g <= std::max(1, CP / 4) && g <= 16; ++g) {

@@ -708,10 +708,11 @@ struct PassCW {
   static constexpr int WARPS = 4;
   static constexpr int CPT = 3;  // combine modes per thread (GPW * Kx <= 3 * 128)
   // prefetch [4][GPW][NX] (F [GPW][4][Kx] overlays it once the FFT inputs are
-  // in registers) | (c1,c2) [GPW][Kx] | xbuf per group | kx [Kx] | mbarrier
+  // in registers) | (c1,c2) [GPW][Kx] | xbuf per group | mbarrier
+  // (kx is read from the L1-resident global table: 4 CTAs/SM fit)
   static size_t bytes(int Kx) {
     return (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * Kx * sizeof(double2) +
-           (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) + (size_t)Kx * sizeof(double) + 8;
+           (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) + 8;
   }
 };
 
@@ -722,7 +723,7 @@ struct PassCW {
 // thread combines its modes (flux divergence, e^{-sL}, weight) into register
 // accumulators, which are added to the group's slot once at the end.
 template <int NX>
-__global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
+__global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
     passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
                  const double2* __restrict__ ctab, double2* __restrict__ slots, int first_chunk) {
   using W = PassCW<NX>;
@@ -734,8 +735,7 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   double2* F = pre;                                    // [GPW][4][Kx], overlays pre
   double2* ctb = pre + (size_t)4 * GPW * NX;           // [GPW][Kx]
   double* xbuf = reinterpret_cast<double*>(ctb + (size_t)GPW * Kx);
-  double* kxs = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(kxs + Kx);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF);
   const int cols = (Ky + GPW - 1) / GPW;
   const int cb = blockIdx.x % cols, g = blockIdx.x / cols;
   const int lo = (int)(((long long)g * np) / Gc), hi = (int)(((long long)(g + 1) * np) / Gc);
@@ -744,7 +744,6 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   const int ncol = min(GPW, Ky - j0);  // active columns of this CTA (contiguous in I2)
   const bool tab = ctab != nullptr;
   const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < Kx; i += blockDim.x) kxs[i] = G.kxc[i];
 
   // warp 0: lane 0 posts the byte count, lanes 0..4 each issue one bulk copy
   // (the CTA's ncol columns of field f are contiguous in I2)
@@ -795,7 +794,7 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
       const int tt = idx / Kx, r = idx % Kx;
       if (tt < ncol) {
         const double2* Ft = F + (size_t)tt * 4 * Kx;
-        const double kx = kxs[r], ky = G.kyc[j0 + tt];
+        const double kx = __ldg(G.kxc + r), ky = G.kyc[j0 + tt];
         const double2 gx = cik(kx, Ft[2 * Kx + r]), gy = cik(ky, Ft[3 * Kx + r]);
         C3 q = {Ft[r], Ft[Kx + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
         if (tab) {
