@@ -194,10 +194,21 @@ def download_fields(tensors):
     return [_POOL_OUT.array(h) for h in hosts]
 
 
+def _side_stream(torch, device):
+    """This (pool) thread's own CUDA stream for upload copies."""
+    st = getattr(_PIN, "side", None)
+    if st is None:
+        st = torch.cuda.Stream(device=device)
+        _PIN.side = st
+    return st
+
+
 def upload_fields(arrays, device: int):
-    """Host fields -> CUDA tensors: parallel host copies into a reused pinned
-    staging buffer, then async H2D copies on the current stream.  The buffer
-    is rewritten only after the previous upload's copies completed."""
+    """Host fields -> CUDA tensors.  Each field is copied into its slot of a
+    reused pinned staging buffer by a worker thread, which then queues that
+    slot's H2D copy on its own stream -- field i's DMA overlaps field i+1's
+    host copy; the caller's stream waits for all of them.  A slot is
+    rewritten only after its previous copy completed."""
     torch = _torch()
     arrays = [np.asarray(a) for a in arrays]
     shape = arrays[0].shape
@@ -206,25 +217,31 @@ def upload_fields(arrays, device: int):
     ent = cache.get(key)
     if ent is None:
         pin = torch.empty((len(arrays),) + shape, dtype=torch.complex128, pin_memory=True)
-        ent = [pin, pin.numpy(), None]
+        ent = [pin, pin.numpy(), [None] * len(arrays)]
         cache[key] = ent
-    pin, pn, ev = ent
-    if ev is not None:
-        ev.synchronize()
+    pin, pn, evs = ent
+    dev = torch.device("cuda", device)
+    out = [torch.empty(shape, dtype=torch.complex128, device=dev) for _ in arrays]
+    alloc_done = torch.cuda.Event()
+    alloc_done.record()
 
     def put(i):
+        if evs[i] is not None:
+            evs[i].synchronize()
         np.copyto(pn[i], arrays[i], casting="same_kind")
+        st = _side_stream(torch, device)
+        st.wait_event(alloc_done)
+        with torch.cuda.stream(st):
+            out[i].copy_(pin[i], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        return ev
 
-    list(_copy_pool().map(put, range(len(arrays))))
-    dev = torch.device("cuda", device)
-    out = []
-    for i in range(len(arrays)):
-        t = torch.empty(shape, dtype=torch.complex128, device=dev)
-        t.copy_(pin[i], non_blocking=True)
-        out.append(t)
-    ev = torch.cuda.Event()
-    ev.record()
-    ent[2] = ev
+    new = list(_copy_pool().map(put, range(len(arrays))))
+    cur = torch.cuda.current_stream()
+    for i, ev in enumerate(new):
+        cur.wait_event(ev)
+        evs[i] = ev
     return out
 
 
