@@ -295,12 +295,18 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
           double2 recv;
           recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
           recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
-          q[cc] = h ? recv : sv;
-          q[8 + cc] = h ? (INV ? cmk(-dv.y, dv.x) : cmk(dv.y, -dv.x)) : recv;
+          // The odd lane keeps its DFT16 input rotated by 8 registers
+          // (received value in the upper half for both lanes: one select
+          // instead of two); the rotation multiplies its output k by (-1)^k,
+          // undone by negating the twiddle base below.
+          q[cc] = h ? (INV ? cmk(-dv.y, dv.x) : cmk(dv.y, -dv.x)) : sv;
+          q[8 + cc] = recv;
         }
-        dft16<INV>(q);  // Z[n1][2 q' + h] (the odd lane's already times W^{n1})
+        dft16<INV>(q);  // Z[n1][2 q' + h] (the odd lane's times W^{n1} (-1)^q')
         // twiddle W_N^{n1 (2q'+h)} = W^{n1 h} (W^{2 n1})^{q'}
-        apply_powers<16>(q, wsel(wl.w2n1(), INV));
+        double2 wb = wsel(wl.w2n1(), INV);
+        if (h) wb = cmk(-wb.x, -wb.y);
+        apply_powers<16>(q, wb);
         PSWE_XPOSE(
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].x,
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].y,
