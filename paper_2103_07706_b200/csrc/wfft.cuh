@@ -138,6 +138,23 @@ __device__ __forceinline__ void apply_powers(double2* v, double2 w) {
   }
 }
 
+// v[k] *= s w^k with s = -1 if neg else 1 (the sign rides on the power chains)
+template <int L>
+__device__ __forceinline__ void apply_powers_neg(double2* v, double2 w, bool neg) {
+  const double2 w2 = cmul(w, w);
+  double2 po = neg ? cmk(-w.x, -w.y) : w, pe = neg ? cmk(-w2.x, -w2.y) : w2;
+  v[0] = neg ? cmk(-v[0].x, -v[0].y) : v[0];
+#pragma unroll
+  for (int k = 1; k < L; k += 2) {
+    v[k] = cmul(v[k], po);
+    po = cmul(po, w2);
+    if (k + 1 < L) {
+      v[k + 1] = cmul(v[k + 1], pe);
+      pe = cmul(pe, w2);
+    }
+  }
+}
+
 // twiddle table of one transform length N: W_N^k, k = 0..N-1 (forward sign);
 // the FFT reads per-lane bases from it and generates powers in registers.
 struct WTab {
@@ -214,8 +231,15 @@ __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WLa
   } else {
     constexpr int T = WF<N>::T, S = WF<N>::S;
     dft16<INV, BAND && (N >= 64)>(v);
-    if constexpr (T > 1) {
+    if constexpr (T == 32) {
+      // W_N^{t k1}, and every value of a lane t = 3 (mod 4) negated: the odd
+      // reader's inputs m then carry (-1)^m, so its DFT16 output comes out
+      // rotated by 8 registers (see the exchange below)
+      apply_powers_neg<16>(v, wsel(wl.wt(), INV), (t & 3) == 3);
+    } else if constexpr (T > 1) {
       apply_powers<16>(v, wsel(wl.wt(), INV));  // W_N^{t k1}
+    }
+    if constexpr (T > 1) {
       if constexpr (T <= 16) {
         constexpr int C = 16 / T;
         PSWE_XPOSE(
@@ -232,18 +256,19 @@ __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WLa
             for (int q = 0; q < 16; ++q) xb[q * S + t] = v[q].y,
             for (int m = 0; m < 16; ++m) v[m].x = xb[k1 * S + h + 2 * m],
             for (int m = 0; m < 16; ++m) v[m].y = xb[k1 * S + h + 2 * m])
-        dft16<INV>(v);  // E_h[k2'], k2' = 0..15
+        // E_h[k2'], k2' = 0..15; the odd lane's rotated: v[i] = E_1[(i + 8) % 16]
+        dft16<INV>(v);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const double2 send = h ? v[c] : v[8 + c];
+          // even lane sends E_0[8 + c], odd lane E_1[c]: both v[8 + c]
           double2 recv;
-          recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
-          recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+          recv.x = __shfl_xor_sync(0xffffffffu, v[8 + c].x, 1);
+          recv.y = __shfl_xor_sync(0xffffffffu, v[8 + c].y, 1);
           const double2 e0 = h ? recv : v[c];
           // W_32^{8+c} = W_32^c W_32^8 and W_32^8 = +-i: the odd lane's operand
-          // is rotated (a register swap + sign) and the twiddle is the
-          // lane-uniform constant W_32^c
-          const double2 o = v[8 + c];
+          // E_1[8 + c] = v[c] is rotated (a register swap + sign) and the
+          // twiddle is the lane-uniform constant W_32^c
+          const double2 o = v[c];
           const double2 e1 = h ? (INV ? cmk(-o.y, o.x) : cmk(o.y, -o.x)) : recv;
           const double2 we1 = cmul(w32(c, INV), e1);
           v[c] = cadd(e0, we1);
