@@ -716,6 +716,10 @@ struct PassCW {
   }
 };
 
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // CTA = (GPW ky columns) x (phase group g of the chunk).  Loops over the
 // group's phases in ascending order; each phase's 4 product columns
 // (contiguous in I2) and its phase-table columns are TMA-bulk-prefetched
@@ -757,6 +761,14 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
       bulk_g2s(pre + (size_t)lane * GPW * NX, I2 + ((size_t)pl * 4 + lane) * KyNX + (size_t)j0 * NX, seg, bar);
     if (lane == 4 && tab) bulk_g2s(ctb, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg, bar);
   };
+  // pull phase pl's bytes into L2 while the previous phase computes, so the
+  // shared-memory fill issued after its combine is an L2 round trip
+  auto warm = [&](int pl) {
+    const uint32_t seg = (uint32_t)(ncol * NX * sizeof(double2));
+    const uint32_t tseg = (uint32_t)(ncol * Kx * sizeof(double2));
+    if (lane < 4) bulk_prefetch_l2(I2 + ((size_t)pl * 4 + lane) * KyNX + (size_t)j0 * NX, seg);
+    if (lane == 4 && tab) bulk_prefetch_l2(ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg);
+  };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -779,6 +791,7 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
 #pragma unroll
     for (int n1 = 0; n1 < P; ++n1) v[n1] = mine[t + T * n1];
     __syncthreads();  // every warp holds its inputs: F may overwrite pre
+    if (f == 0 && pl + 1 < hi) warm(pl + 1);
     // (the combine below reads F and ctb, so the refill waits for the end of this phase)
     wfft_t1<NX, false>(v, t, xb, wl);
 #pragma unroll
