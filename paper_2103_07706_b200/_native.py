@@ -123,15 +123,6 @@ def _stream(torch):
 
 
 _PIN = threading.local()  # per-thread pinned staging buffers for uploads
-_POOL = None
-
-
-def _copy_pool():
-    global _POOL
-    if _POOL is None:
-        from concurrent.futures import ThreadPoolExecutor
-        _POOL = ThreadPoolExecutor(max_workers=3, thread_name_prefix="pswe-copy")
-    return _POOL
 
 
 class _PinnedPool:
@@ -194,21 +185,12 @@ def download_fields(tensors):
     return [_POOL_OUT.array(h) for h in hosts]
 
 
-def _side_stream(torch, device):
-    """This (pool) thread's own CUDA stream for upload copies."""
-    st = getattr(_PIN, "side", None)
-    if st is None:
-        st = torch.cuda.Stream(device=device)
-        _PIN.side = st
-    return st
-
-
 def upload_fields(arrays, device: int):
-    """Host fields -> CUDA tensors.  Each field is copied into its slot of a
-    reused pinned staging buffer by a worker thread, which then queues that
-    slot's H2D copy on its own stream -- field i's DMA overlaps field i+1's
-    host copy; the caller's stream waits for all of them.  A slot is
-    rewritten only after its previous copy completed."""
+    """Host fields -> CUDA tensors through a reused pinned staging buffer:
+    field i is copied into its slot by torch's multi-threaded host copy, then
+    its H2D copy is queued on the caller's stream, so field i's DMA overlaps
+    field i+1's host copy.  A slot is rewritten only after its previous DMA
+    completed."""
     torch = _torch()
     arrays = [np.asarray(a) for a in arrays]
     shape = arrays[0].shape
@@ -221,28 +203,20 @@ def upload_fields(arrays, device: int):
         cache[key] = ent
     pin, pn, evs = ent
     dev = torch.device("cuda", device)
-    out = [torch.empty(shape, dtype=torch.complex128, device=dev) for _ in arrays]
-    alloc_done = torch.cuda.Event()
-    alloc_done.record()
-
-    def put(i):
+    out = torch.empty((len(arrays),) + shape, dtype=torch.complex128, device=dev)
+    cur = torch.cuda.current_stream(dev)
+    for i, a in enumerate(arrays):
         if evs[i] is not None:
             evs[i].synchronize()
-        np.copyto(pn[i], arrays[i], casting="same_kind")
-        st = _side_stream(torch, device)
-        st.wait_event(alloc_done)
-        with torch.cuda.stream(st):
-            out[i].copy_(pin[i], non_blocking=True)
+        if a.dtype == np.complex128 and a.flags.writeable and all(st >= 0 for st in a.strides):
+            pin[i].copy_(torch.from_numpy(a))
+        else:  # read-only / negative strides / other dtypes: numpy's copy
+            np.copyto(pn[i], a, casting="same_kind")
+        out[i].copy_(pin[i], non_blocking=True)
         ev = torch.cuda.Event()
-        ev.record(st)
-        return ev
-
-    new = list(_copy_pool().map(put, range(len(arrays))))
-    cur = torch.cuda.current_stream()
-    for i, ev in enumerate(new):
-        cur.wait_event(ev)
+        ev.record(cur)
         evs[i] = ev
-    return out
+    return [out[i] for i in range(len(arrays))]
 
 
 class Context:

@@ -750,6 +750,20 @@ int pswe_set_quadrature(pswe_ctx* c, int n_nodes, const double* s, const double*
   if (!c || !s || !w) return set_err(PSWE_EINVAL, "null argument");
   if (n_nodes < 1 || n_nodes % 2 != 1) return set_err(PSWE_EINVAL, "need an odd number of nodes (2M+1), got %d", n_nodes);
   CU(cudaSetDevice(c->device));
+  {
+    // the same quadrature again (a caller that sets it before every
+    // evaluation): keep the device arrays and the phase table
+    std::vector<double> s2, w2;
+    std::vector<int> k2;
+    const int M = (n_nodes - 1) / 2;
+    for (int i = 0; i < n_nodes; ++i)
+      if (w[i] != 0.0) {
+        s2.push_back(s[i]);
+        w2.push_back(w[i]);
+        k2.push_back(i - M);
+      }
+    if (c->quad_set && M == c->M && s2 == c->s_live && w2 == c->w_live && k2 == c->k_live) return PSWE_OK;
+  }
   c->M = (n_nodes - 1) / 2;
   c->s_live.clear();
   c->w_live.clear();
