@@ -144,7 +144,8 @@ int pswe_diagnostics(pswe_ctx* ctx, const double* u_dev, const double* v_dev, co
 int pswe_to_physical(pswe_ctx* ctx, const double* u_dev, const double* v_dev, const double* eta_dev,
                      double* phys_dev, void* stream);
 
-/* Tuning: bytes of chunk intermediates per lane (default 1536 MiB, four lanes). */
+/* Tuning: bytes of chunk intermediates per chunk (default 2048 MiB; at least
+ * one chunk per lane). */
 int pswe_set_chunk_bytes(pswe_ctx* ctx, size_t bytes);
 
 /* Tuning: chunk lanes (streams whose chunks overlap), 1..4, default 4. */

@@ -103,7 +103,7 @@ struct pswe_ctx {
   double Lambda = 0;
   DevBuf<double> a_dev;
   // scratch
-  size_t chunk_bytes = size_t(1536) << 20;
+  size_t chunk_bytes = size_t(2048) << 20;
   DevBuf<double2> inter, slots, Uc, Ac, Ac2;
   static constexpr int MAX_LANES = 4;
   cudaStream_t st_lane[MAX_LANES - 1] = {};  // chunk lanes 1.. (lane 0 is the caller's stream)
@@ -431,7 +431,11 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   // multiple of `lanes` equal chunks no larger than chunk_bytes, so the lanes
   // finish together.
   const int cpmax = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
-  int nchunks = (P + cpmax - 1) / cpmax;
+  // at least one chunk per lane when a chunk still holds >= 16 phases and
+  // >= 24 MiB of intermediates: the lanes' overlap is then worth more than
+  // the larger per-launch grids of fewer chunks
+  const int minph = std::max<int>(16, (int)((size_t(24) << 20) / (per_phase * sizeof(double2))));
+  int nchunks = std::max((P + cpmax - 1) / cpmax, std::min(c->n_lanes, P / minph));
   const int lanes = std::max(1, std::min(c->n_lanes, nchunks));
   nchunks = (nchunks + lanes - 1) / lanes * lanes;
   const int CP = std::max(1, std::min(P, (P + nchunks - 1) / nchunks));

@@ -20,6 +20,10 @@ __device__ __forceinline__ double2 cscale(double s, double2 a) { return cmk(s * 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+// c + w y with the products fused: two FMAs per component
+__device__ __forceinline__ double2 cfma(double2 w, double2 y, double2 c) {
+  return cmk(fma(w.x, y.x, fma(-w.y, y.y, c.x)), fma(w.x, y.y, fma(w.y, y.x, c.y)));
+}
 __device__ __forceinline__ double2 cconj(double2 a) { return cmk(a.x, -a.y); }
 // i * a
 __device__ __forceinline__ double2 cmuli(double2 a) { return cmk(-a.y, a.x); }

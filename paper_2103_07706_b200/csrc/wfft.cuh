@@ -90,21 +90,33 @@ __device__ __forceinline__ void dft16(double2* v) {
     a[n2][2] = y2;
     a[n2][3] = y3;
   }
-#pragma unroll
-  for (int n2 = 1; n2 < 4; ++n2)
-#pragma unroll
-    for (int k1 = 1; k1 < 4; ++k1) {
-      const int e = n2 * k1;
-      if (e == 4) {
-        a[n2][k1] = INV ? cmuli(a[n2][k1]) : cmk(a[n2][k1].y, -a[n2][k1].x);
-      } else {
-        a[n2][k1] = cmul(a[n2][k1], w16(e, INV));
-      }
-    }
+  // second layer: dft4 over n2 of a[n2][k1] W_16^{n2 k1}, the twiddle
+  // products fused into the first butterflies (x + w y as two FMAs per
+  // component, x - w y as 2x - (x + w y))
 #pragma unroll
   for (int k1 = 0; k1 < 4; ++k1) {
     double2 y0 = a[0][k1], y1 = a[1][k1], y2 = a[2][k1], y3 = a[3][k1];
-    dft4<INV>(y0, y1, y2, y3);
+    if (k1 == 0) {
+      dft4<INV>(y0, y1, y2, y3);
+    } else {
+      double2 s0, d0;
+      if (k1 == 2) {  // W_16^4 = -+i: a register swap + sign
+        const double2 t = INV ? cmuli(y2) : cmk(y2.y, -y2.x);
+        s0 = cadd(y0, t);
+        d0 = csub(y0, t);
+      } else {
+        s0 = cfma(w16(2 * k1, INV), y2, y0);
+        d0 = cmk(fma(2.0, y0.x, -s0.x), fma(2.0, y0.y, -s0.y));
+      }
+      const double2 p1 = cmul(y1, w16(k1, INV));
+      const double2 s1 = cfma(w16(3 * k1, INV), y3, p1);
+      const double2 d1 = cmk(fma(2.0, p1.x, -s1.x), fma(2.0, p1.y, -s1.y));
+      const double2 r = INV ? cmk(-d1.y, d1.x) : cmk(d1.y, -d1.x);
+      y0 = cadd(s0, s1);
+      y2 = csub(s0, s1);
+      y1 = cadd(d0, r);
+      y3 = csub(d0, r);
+    }
     v[k1] = y0;
     v[k1 + 4] = y1;
     v[k1 + 8] = y2;
