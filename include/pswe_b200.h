@@ -144,6 +144,16 @@ int pswe_diagnostics(pswe_ctx* ctx, const double* u_dev, const double* v_dev, co
 int pswe_to_physical(pswe_ctx* ctx, const double* u_dev, const double* v_dev, const double* eta_dev,
                      double* phys_dev, void* stream);
 
+/* Transfer helper of the drop-in path (no reference counterpart: the
+ * reference's fields live in host memory).  Copies only the 2/3 band of
+ * nfields full-layout fields -- rows |kx| <= nx/3 and columns |ky| <= ny/3,
+ * everything pack reads and everything unpack can write nonzero -- host to
+ * device (dir 0) or device to host (dir 1), asynchronously on the stream
+ * (host buffers should be pinned).  Entries outside the band are not
+ * touched. */
+int pswe_copy_band(pswe_ctx* ctx, int dir, double* const* dst, const double* const* src, int nfields,
+                   void* stream);
+
 /* Tuning: bytes of chunk intermediates per chunk (default 2048 MiB; at least
  * one chunk per lane). */
 int pswe_set_chunk_bytes(pswe_ctx* ctx, size_t bytes);

@@ -57,6 +57,7 @@ SIGNATURES = {
     "pswe_launch_count": (ctypes.c_int64, [_vp]),
     "pswe_diagnostics": (_i, [_vp, _vp, _vp, _vp, ctypes.POINTER(_d), _vp]),
     "pswe_to_physical": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pswe_copy_band": (_i, [_vp, _i, _vp, _vp, _i, _vp]),
     "pswe_set_chunk_bytes": (_i, [_vp, ctypes.c_size_t]),
     "pswe_set_lanes": (_i, [_vp, _i]),
     "pswe_get_lanes": (_i, [_vp]),
@@ -172,25 +173,61 @@ class _PinnedHolder:
 _POOL_OUT = _PinnedPool()
 
 
-def download_fields(tensors):
+def band_blocks(nx: int, ny: int):
+    """(row slice, column slice) blocks of the 2/3 band of a full (nx, ny)
+    field: |kx| <= nx/3, |ky| <= ny/3 (grid.py:102-103)."""
+    kxm, kym = nx // 3, ny // 3
+    rows = (slice(0, kxm + 1), slice(nx - kxm, nx))
+    cols = (slice(0, kym + 1), slice(ny - kym, ny))
+    return [(r, c) for r in rows for c in cols]
+
+
+def band_bytes(nx: int, ny: int) -> int:
+    """Bytes of one complex128 field's 2/3 band (what a band copy moves)."""
+    return (2 * (nx // 3) + 1) * (2 * (ny // 3) + 1) * 16
+
+
+def _ptrs(xs):
+    return (ctypes.c_void_p * len(xs))(*xs)
+
+
+def _zero_out_of_band(h, nx, ny):
+    kxm, kym = nx // 3, ny // 3
+    h[kxm + 1:nx - kxm].zero_()
+    h[:kxm + 1, kym + 1:ny - kym].zero_()
+    h[nx - kxm:, kym + 1:ny - kym].zero_()
+
+
+def download_fields(tensors, band_ctx=None):
     """CUDA tensors -> numpy arrays backed by pooled pinned host memory (one
-    stream sync, no host copy)."""
+    stream sync, no host copy).  With ``band_ctx`` (a Context) the tensors are
+    known to vanish outside the 2/3 band: only the band crosses the bus and
+    the host zero-fills the rest (before the copy is queued, while the device
+    is still busy)."""
     torch = _torch()
-    hosts = []
-    for t in tensors:
-        h = _POOL_OUT.take(t.shape, t.dtype)
-        h.copy_(t, non_blocking=True)
-        hosts.append(h)
+    hosts = [_POOL_OUT.take(t.shape, t.dtype) for t in tensors]
+    if band_ctx is not None and tensors:
+        nx, ny = tensors[0].shape
+        for h in hosts:
+            _zero_out_of_band(h, nx, ny)
+        _check(_lib.pswe_copy_band(band_ctx.h, 1, _ptrs([h.data_ptr() for h in hosts]),
+                                   _ptrs([t.data_ptr() for t in tensors]), len(tensors), _stream(torch)))
+    else:
+        for h, t in zip(hosts, tensors):
+            h.copy_(t, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return [_POOL_OUT.array(h) for h in hosts]
 
 
-def upload_fields(arrays, device: int):
+def upload_fields(arrays, device: int, band_ctx=None):
     """Host fields -> CUDA tensors through a reused pinned staging buffer:
     field i is copied into its slot by torch's multi-threaded host copy, then
     its H2D copy is queued on the caller's stream, so field i's DMA overlaps
     field i+1's host copy.  A slot is rewritten only after its previous DMA
-    completed."""
+    completed.  With ``band_ctx`` (a Context) only the 2/3 band is staged and
+    copied -- for consumers that read nothing else (pack, i.e. the averaged
+    tendency, which truncates its input to the band first, dynamics.py:
+    153-156); the device tensors are undefined outside the band."""
     torch = _torch()
     arrays = [np.asarray(a) for a in arrays]
     shape = arrays[0].shape
@@ -205,14 +242,25 @@ def upload_fields(arrays, device: int):
     dev = torch.device("cuda", device)
     out = torch.empty((len(arrays),) + shape, dtype=torch.complex128, device=dev)
     cur = torch.cuda.current_stream(dev)
+    # staged on the host: whole fields (one threaded copy per field costs
+    # less than several copies of the band's blocks -- the copies are
+    # dispatch-bound); on the bus: the band only
+    blocks = [(slice(None), slice(None))]
     for i, a in enumerate(arrays):
         if evs[i] is not None:
             evs[i].synchronize()
-        if a.dtype == np.complex128 and a.flags.writeable and all(st >= 0 for st in a.strides):
-            pin[i].copy_(torch.from_numpy(a))
-        else:  # read-only / negative strides / other dtypes: numpy's copy
-            np.copyto(pn[i], a, casting="same_kind")
-        out[i].copy_(pin[i], non_blocking=True)
+        fast = a.dtype == np.complex128 and a.flags.writeable and all(st >= 0 for st in a.strides)
+        src = torch.from_numpy(a) if fast else None
+        for r, c in blocks:
+            if fast:
+                pin[i, r, c].copy_(src[r, c])
+            else:  # read-only / negative strides / other dtypes: numpy's copy
+                np.copyto(pn[i, r, c], a[r, c], casting="same_kind")
+        if band_ctx is not None:
+            _check(_lib.pswe_copy_band(band_ctx.h, 0, _ptrs([out[i].data_ptr()]), _ptrs([pin[i].data_ptr()]), 1,
+                                       ctypes.c_void_p(cur.cuda_stream)))
+        else:
+            out[i].copy_(pin[i], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(cur)
         evs[i] = ev

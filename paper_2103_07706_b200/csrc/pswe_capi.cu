@@ -1054,6 +1054,28 @@ int pswe_to_physical(pswe_ctx* c, const double* u, const double* v, const double
   return physical_fields(c, u, v, e, phys, (cudaStream_t)stream);
 }
 
+int pswe_copy_band(pswe_ctx* c, int dir, double* const* dst, const double* const* src, int nfields,
+                   void* stream) {
+  if (!c || !dst || !src || nfields < 0) return set_err(PSWE_EINVAL, "null argument");
+  if (dir != 0 && dir != 1) return set_err(PSWE_EINVAL, "dir must be 0 (host to device) or 1 (device to host)");
+  CU(cudaSetDevice(c->device));
+  const cudaMemcpyKind kind = dir == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  const size_t pitch = (size_t)c->ny * 2 * sizeof(double);
+  // rows |wx| <= kxm and columns |wy| <= kym: two row blocks x two column blocks
+  const int r0[2] = {0, c->nx - c->kxm}, nr[2] = {c->kxm + 1, c->kxm};
+  const int c0[2] = {0, c->ny - c->kym}, nc[2] = {c->kym + 1, c->kym};
+  for (int f = 0; f < nfields; ++f) {
+    if (!dst[f] || !src[f]) return set_err(PSWE_EINVAL, "null field pointer");
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        const size_t off = ((size_t)r0[a] * c->ny + c0[b]) * 2;
+        CU(cudaMemcpy2DAsync(dst[f] + off, pitch, src[f] + off, pitch, (size_t)nc[b] * 2 * sizeof(double), nr[a],
+                             kind, (cudaStream_t)stream));
+      }
+  }
+  return PSWE_OK;
+}
+
 int pswe_diagnostics(pswe_ctx* c, const double* u, const double* v, const double* e, double* out3,
                                 void* stream) {
   if (!c || !u || !v || !e || !out3) return set_err(PSWE_EINVAL, "null argument");

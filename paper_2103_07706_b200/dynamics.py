@@ -111,19 +111,23 @@ def context(state_or_grid, params):
     return ctx
 
 
-def upload(ctx, state):
+def upload(ctx, state, band: bool = False):
+    """State fields -> device tensors.  ``band``: only the 2/3 band is
+    copied (for consumers that truncate their input to it first)."""
     fields = [getattr(state, n) for n in ("u", "v", "eta")]
     if any(not isinstance(a, np.ndarray) for a in fields):
         return [ctx.to_device(a) for a in fields]
     for a in fields:
         if a.shape != (ctx.nx, ctx.ny):
             raise ValueError(f"field shape {a.shape} does not match the grid ({ctx.nx}, {ctx.ny})")
-    return _native.upload_fields(fields, ctx.device)
+    return _native.upload_fields(fields, ctx.device, band_ctx=ctx if band else None)
 
 
-def download(tensors):
+def download(tensors, band_ctx=None):
+    """Device tensors -> numpy.  ``band_ctx``: the tensors vanish outside the
+    2/3 band (a dealiased tendency), so only the band is copied back."""
     if tensors and tensors[0].is_cuda:
-        return _native.download_fields(tensors)
+        return _native.download_fields(tensors, band_ctx=band_ctx)
     return [t.numpy() for t in tensors]
 
 
