@@ -707,39 +707,42 @@ struct PassCW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 4;
   static constexpr int CPT = 3;  // combine modes per thread (GPW * Kx <= 3 * 128)
-  // prefetch [4][GPW][NX] (F [GPW][4][Kx] overlays it once the FFT inputs are
-  // in registers) | (c1,c2) [GPW][Kx] | xbuf per group | mbarrier
-  // (kx is read from the L1-resident global table: 4 CTAs/SM fit)
-  static size_t bytes(int Kx) {
-    return (size_t)4 * GPW * NX * sizeof(double2) + (size_t)GPW * Kx * sizeof(double2) +
-           (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) + 8;
+  static constexpr int Kx = 2 * (NX / 3) + 1;
+  // a transform's exchange buffer fits in its own input column once the
+  // column is in registers (all but the 16-point transform)
+  static constexpr bool XB_IN_PRE = WF<NX>::XBUF * sizeof(double) <= NX * sizeof(double2);
+  // double-buffered: prefetch [2][4][GPW][NX] (each transform's band output
+  // F and exchange buffer overlay its own input column) | (c1,c2) [2][GPW][Kx]
+  // | [xbuf per group] | mbarrier [2]
+  static size_t bytes(int) {
+    return (size_t)2 * 4 * GPW * NX * sizeof(double2) + (size_t)2 * GPW * Kx * sizeof(double2) +
+           (XB_IN_PRE ? 0 : (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double)) + 16;
   }
 };
 
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
 // CTA = (GPW ky columns) x (phase group g of the chunk).  Loops over the
-// group's phases in ascending order; each phase's 4 product columns
-// (contiguous in I2) and its phase-table columns are TMA-bulk-prefetched
-// while the previous phase computes.  Warp f transforms field f; then every
-// thread combines its modes (flux divergence, e^{-sL}, weight) into register
-// accumulators, which are added to the group's slot once at the end.
+// group's phases in ascending order with two buffers: phase pl's 4 product
+// columns (contiguous in I2) and phase-table columns are TMA-bulk-copied
+// while phase pl - 1 computes (a whole phase of lead).  Warp f transforms
+// field f in its own column of the buffer (exchange buffer and band output
+// overlay the consumed input); then every thread combines its modes (flux
+// divergence, e^{-sL}, weight) into register accumulators, which are added
+// to the group's slot once at the end.
 template <int NX>
-__global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
+__global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
     passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
                  const double2* __restrict__ ctab, double2* __restrict__ slots, int first_chunk) {
   using W = PassCW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, CPT = W::CPT;
   extern __shared__ __align__(128) unsigned char sbytes[];
-  constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
+  constexpr int Kx = W::Kx;  // == G.Kx
+  constexpr size_t PB = (size_t)4 * GPW * NX;  // double2 per prefetch buffer
   const int Ky = G.Ky;
-  double2* pre = reinterpret_cast<double2*>(sbytes);  // [4][GPW][NX]
-  double2* F = pre;                                    // [GPW][4][Kx], overlays pre
-  double2* ctb = pre + (size_t)4 * GPW * NX;           // [GPW][Kx]
-  double* xbuf = reinterpret_cast<double*>(ctb + (size_t)GPW * Kx);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF);
+  double2* pre0 = reinterpret_cast<double2*>(sbytes);  // [2][4][GPW][NX]
+  double2* ctb0 = pre0 + 2 * PB;                       // [2][GPW][Kx]
+  double* xbuf = reinterpret_cast<double*>(ctb0 + (size_t)2 * GPW * Kx);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(
+      xbuf + (W::XB_IN_PRE ? 0 : (size_t)W::WARPS * GPW * WF<NX>::XBUF));  // [2]
   const int cols = (Ky + GPW - 1) / GPW;
   const int cb = blockIdx.x % cols, g = blockIdx.x / cols;
   const int lo = (int)(((long long)g * np) / Gc), hi = (int)(((long long)(g + 1) * np) / Gc);
@@ -753,47 +756,48 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
   // (the CTA's ncol columns of field f are contiguous in I2)
   const size_t KyNX = (size_t)Ky * NX;
   auto prefetch = [&](int pl) {
+    const int b = (pl - lo) & 1;
     const uint32_t seg = (uint32_t)(ncol * NX * sizeof(double2));
     const uint32_t tseg = (uint32_t)(ncol * Kx * sizeof(double2));
-    if (lane == 0) mbar_arrive_expect_tx(bar, 4 * seg + (tab ? tseg : 0));
+    if (lane == 0) mbar_arrive_expect_tx(bar + b, 4 * seg + (tab ? tseg : 0));
     __syncwarp();
     if (lane < 4)
-      bulk_g2s(pre + (size_t)lane * GPW * NX, I2 + ((size_t)pl * 4 + lane) * KyNX + (size_t)j0 * NX, seg, bar);
-    if (lane == 4 && tab) bulk_g2s(ctb, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg, bar);
-  };
-  // pull phase pl's bytes into L2 while the previous phase computes, so the
-  // shared-memory fill issued after its combine is an L2 round trip
-  auto warm = [&](int pl) {
-    const uint32_t seg = (uint32_t)(ncol * NX * sizeof(double2));
-    const uint32_t tseg = (uint32_t)(ncol * Kx * sizeof(double2));
-    if (lane < 4) bulk_prefetch_l2(I2 + ((size_t)pl * 4 + lane) * KyNX + (size_t)j0 * NX, seg);
-    if (lane == 4 && tab) bulk_prefetch_l2(ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg);
+      bulk_g2s(pre0 + b * PB + (size_t)lane * GPW * NX, I2 + ((size_t)pl * 4 + lane) * KyNX + (size_t)j0 * NX, seg,
+               bar + b);
+    if (lane == 4 && tab)
+      bulk_g2s(ctb0 + (size_t)b * GPW * Kx, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, tseg, bar + b);
   };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (f == 0 && lo < hi) prefetch(lo);
+  if (f == 0) {
+    if (lo < hi) prefetch(lo);
+    if (lo + 1 < hi) prefetch(lo + 1);
+  }
 
   const int tl = lane / T, t = lane % T;
-  double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
-  double2* Ff = F + ((size_t)tl * 4 + f) * Kx;
-  const double2* mine = pre + ((size_t)f * GPW + tl) * NX;
+  const size_t own = ((size_t)f * GPW + tl) * NX;  // this transform's column in a buffer
   const WLane wl = wlane<NX>(G.twx, t);
   C3 acc[CPT];
 #pragma unroll
   for (int c = 0; c < CPT; ++c) acc[c] = c3zero();
 #pragma unroll 1
   for (int pl = lo; pl < hi; ++pl) {
-    mbar_wait(bar, (pl - lo) & 1);
+    const int b = (pl - lo) & 1;
+    double2* pre = pre0 + b * PB;
+    mbar_wait(bar + b, ((pl - lo) >> 1) & 1);
     double2 v[P];
 #pragma unroll
-    for (int n1 = 0; n1 < P; ++n1) v[n1] = mine[t + T * n1];
-    __syncthreads();  // every warp holds its inputs: F may overwrite pre
-    if (f == 0 && pl + 1 < hi) warm(pl + 1);
-    // (the combine below reads F and ctb, so the refill waits for the end of this phase)
+    for (int n1 = 0; n1 < P; ++n1) v[n1] = pre[own + t + T * n1];
+    __syncwarp();  // the warp's columns are in registers: reuse them
+    double* xb = W::XB_IN_PRE ? reinterpret_cast<double*>(pre + own)
+                              : xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
     wfft_t1<NX, false>(v, t, xb, wl);
+    __syncwarp();  // the exchange buffer's last reads precede the band store
+    double2* Ff = pre + own;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       const int r = band_r(t1_pos<NX>(t, i), NX, NX / 3, Kx);
@@ -801,15 +805,16 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
     }
     __syncthreads();
     const double s = ph.s[p0 + pl], w = ph.w[p0 + pl];
+    const double2* ctb = ctb0 + (size_t)b * GPW * Kx;
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int idx = threadIdx.x + c * W::WARPS * 32;
       const int tt = idx / Kx, r = idx % Kx;
       if (tt < ncol) {
-        const double2* Ft = F + (size_t)tt * 4 * Kx;
+        const double2* Ft = pre + (size_t)tt * NX;  // field f at + f GPW NX
         const double kx = __ldg(G.kxc + r), ky = G.kyc[j0 + tt];
-        const double2 gx = cik(kx, Ft[2 * Kx + r]), gy = cik(ky, Ft[3 * Kx + r]);
-        C3 q = {Ft[r], Ft[Kx + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
+        const double2 gx = cik(kx, Ft[2 * GPW * NX + r]), gy = cik(ky, Ft[3 * GPW * NX + r]);
+        C3 q = {Ft[r], Ft[GPW * NX + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
         if (tab) {
           double2 c12 = ctb[idx];
           c12.x = -c12.x;  // e^{-sL}: c1(-s) = -c1(s), c2(-s) = c2(s)
@@ -820,8 +825,8 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 4)
         acc[c] = c3add(acc[c], c3scale(w, q));
       }
     }
-    __syncthreads();  // pre, ctb and F consumed
-    if (f == 0 && pl + 1 < hi) prefetch(pl + 1);
+    __syncthreads();  // buffer b consumed
+    if (f == 0 && pl + 2 < hi) prefetch(pl + 2);
   }
   // slot (+)= this group's phases, in chunk order
   double2* slot = slots + (size_t)g * 3 * KyKx;
