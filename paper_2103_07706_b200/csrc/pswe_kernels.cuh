@@ -709,8 +709,10 @@ struct PassCW {
   static constexpr int CPT = 3;  // combine modes per thread (GPW * Kx <= 3 * 128)
   static constexpr int Kx = 2 * (NX / 3) + 1;
   // a transform's exchange buffer fits in its own input column once the
-  // column is in registers (all but the 16-point transform)
-  static constexpr bool XB_IN_PRE = WF<NX>::XBUF * sizeof(double) <= NX * sizeof(double2);
+  // column is in registers (NX >= 64), offset by XOFF doubles per group so
+  // the groups of a warp keep XBUF's bank stagger
+  static constexpr bool XB_IN_PRE = WF<NX>::XBUF + 31 <= 2 * NX;
+  static constexpr int XOFF = ((WF<NX>::XBUF - 2 * NX) % 32 + 32) % 32;
   // double-buffered: prefetch [2][4][GPW][NX] (each transform's band output
   // F and exchange buffer overlay its own input column) | (c1,c2) [2][GPW][Kx]
   // | [xbuf per group] | mbarrier [2]
@@ -793,7 +795,7 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
 #pragma unroll
     for (int n1 = 0; n1 < P; ++n1) v[n1] = pre[own + t + T * n1];
     __syncwarp();  // the warp's columns are in registers: reuse them
-    double* xb = W::XB_IN_PRE ? reinterpret_cast<double*>(pre + own)
+    double* xb = W::XB_IN_PRE ? reinterpret_cast<double*>(pre + own) + ((tl * W::XOFF) & 31)
                               : xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
     wfft_t1<NX, false>(v, t, xb, wl);
     __syncwarp();  // the exchange buffer's last reads precede the band store
