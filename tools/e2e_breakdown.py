@@ -17,9 +17,9 @@ n = 5
 for _ in range(n):
     t0 = time.perf_counter(); ctx = dynamics.context(c.state, c.params); propagator.configure(ctx, spec)
     ctx.set_quadrature(c.quadrature.s, c.quadrature.w); mark("setup", t0)
-    t0 = time.perf_counter(); U = dynamics.upload(ctx, c.state); mark("upload", t0)
+    t0 = time.perf_counter(); U = dynamics.upload(ctx, c.state, band=True); mark("upload", t0)
     t0 = time.perf_counter(); out = ctx.averaged_tendency(U); mark("compute", t0)
-    t0 = time.perf_counter(); res = dynamics.download(out); mark("download", t0)
+    t0 = time.perf_counter(); res = dynamics.download(out, band_ctx=ctx); mark("download", t0)
     t0 = time.perf_counter(); st = dynamics.rebuild(c.state, res, c.state.t); mark("rebuild", t0)
     del res, st, out, U
 t0 = time.perf_counter()
