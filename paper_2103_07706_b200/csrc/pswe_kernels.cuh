@@ -172,12 +172,15 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
   const int tl = lane / T, t = lane % T;
   double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
   const WLane wl = wlane<NX>(G.twx, t);
-  int it = 0;
+  // one loop-carried counter (blk derived from it): a second one was spilled
+  // and its reload queued behind the column stores
 #pragma unroll 1
-  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+  for (int it = 0;; ++it) {
+    const int blk = (int)blockIdx.x + it * (int)gridDim.x;
+    if (blk >= nblk) break;
     const int pl = blk / cols, j0 = (blk % cols) * GPW;
     const int ncol = min(GPW, Ky - j0);
-    const double s = ph.s[p0 + pl];
+    const double s = tab ? 0.0 : ph.s[p0 + pl];  // the exact route never reads it
     mbar_wait(bar, it & 1);
     // e^{sL} per mode in place: (u, v, eta, b) -> (u', v', eta' - b) / (nx ny)
     double kyb[GPW];
