@@ -393,11 +393,12 @@ int map_rows_I1(const pswe_ctx* c, double2* I1, int CP, CUtensorMap* m) {
 // warps' column writes into it are bank-conflict free.
 int map_tiles_I2(const pswe_ctx* c, double2* I2, int CP, CUtensorMap* m) {
   const cuuint64_t nx = c->nx, Ky = c->Ky;
-  const cuuint32_t R = (cuuint32_t)std::min<cuuint64_t>(passB_rows(c->ny), nx);
+  const cuuint32_t R = (cuuint32_t)std::min<cuuint64_t>(passB_rows(c->ny) / 2, nx);  // a warp pair's tile
   const cuuint64_t dims[3] = {2 * nx, Ky, (cuuint64_t)4 * CP};
   const cuuint64_t strides[2] = {nx * 16, Ky * nx * 16};
   const cuuint32_t box[3] = {2 * R, (cuuint32_t)Ky, 2};
-  const CUtensorMapSwizzle swz = R == 4 ? CU_TENSOR_MAP_SWIZZLE_64B
+  const CUtensorMapSwizzle swz = R == 2   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : R == 4 ? CU_TENSOR_MAP_SWIZZLE_64B
                                  : (R == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
   return encode_map(m, I2, dims, strides, box, 3, swz);
 }

@@ -255,9 +255,13 @@ struct PassBW {
             (FAST ? 0 : (size_t)GPW * P * T * sizeof(double2)) + 8 + 127) /
            128 * 128;
   }
+  // FAST: each warp pair owns a [2][Ky][RP] staging tile (RP = 2 GPW rows),
+  // synchronised by a named barrier of its 64 threads only
+  static constexpr int RP = 2 * GPW;
+  static constexpr size_t PAIR_STAGE = ((size_t)2 * Ky * RP * sizeof(double2) + 1023) / 1024 * 1024;
   template <bool FAST>
   __host__ __device__ static constexpr size_t stage_bytes() {
-    return FAST ? ((size_t)2 * Ky * R * sizeof(double2) + 127) / 128 * 128 + 1024 : 0;
+    return FAST ? 2 * PAIR_STAGE + 1024 : 0;
   }
   template <bool FAST>
   static size_t bytes() {
@@ -482,7 +486,9 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
 // banks.  Wider tiles are unswizzled.
 template <int NY, int R>
 __device__ __forceinline__ int stage_slot(int line, int rc) {
-  if constexpr (R == 4)
+  if constexpr (R == 2)  // 32-byte lines, SWIZZLE_32B: chunk ^ bit 2 of the line
+    return line * 2 + (rc ^ ((line >> 2) & 1));
+  else if constexpr (R == 4)
     return line * 4 + (rc ^ ((line >> 1) & 3));
   else if constexpr (R == 8)
     return line * 8 + (rc ^ (line & 7));
@@ -547,8 +553,9 @@ template <int NY>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     passB_pair_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mO) {
   using W = PassBW<NY>;
-  constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA, R = W::R;
+  constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA, R = W::R, RP = W::RP;
   static_assert(P == 16, "FAST path needs 16 points per lane");
+  static_assert(W::WARPS == 4, "two warp pairs per CTA");
   extern __shared__ __align__(128) unsigned char sbytes[];
   constexpr int Ky = W::Ky;
   constexpr size_t WB = W::template warp_bytes<true>();
@@ -559,9 +566,12 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   double2* preb = pre + KYA;
   double* xb = reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) + (size_t)g * WF<NY>::XBUF;
   uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + WB - 8);
-  // [2][Ky][R] swizzled staging tile, 1024-byte aligned (swizzle atom)
+  // per warp pair: a [2][Ky][RP] swizzled staging tile, 1024-byte aligned
   const uint32_t stage_pad = (1024u - (smem_u32(sbytes + (size_t)W::WARPS * WB) & 1023u)) & 1023u;
-  double2* stage = reinterpret_cast<double2*>(sbytes + (size_t)W::WARPS * WB + stage_pad);
+  const int pr = warp >> 1, rcp = (warp & 1) * GPW + g;  // pair, row in the pair's tile
+  const bool issuer = (warp & 1) == 0 && lane == 0;       // the pair's TMA-store thread
+  double2* stage =
+      reinterpret_cast<double2*>(sbytes + (size_t)W::WARPS * WB + stage_pad + (size_t)pr * W::PAIR_STAGE);
   double* kys = reinterpret_cast<double*>(sbytes + (size_t)W::WARPS * WB + W::template stage_bytes<true>());
   uint32_t* tslot = reinterpret_cast<uint32_t*>(kys + Ky);
   const int nx = Gd.nx;
@@ -678,18 +688,18 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
       if (it < 2) continue;
       wfft_t2<NY, false>(v, t, xb, wl);
       const int fo = it == 2 ? 0 : 2;
-      if (threadIdx.x == 0) bulk_wait_read0();
-      __syncthreads();
-      unpack_stage<NY, R>(v, t, stage, rc);
+      if (issuer) bulk_wait_read0();
+      named_bar_sync(1 + pr, 64);
+      unpack_stage<NY, RP>(v, t, stage, rcp);
       fence_proxy_async();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tma_store_3d(&mO, 2 * x0, 0, 4 * (p0 + sub) + fo, stage);
+      named_bar_sync(1 + pr, 64);
+      if (issuer) {
+        tma_store_3d(&mO, 2 * (x0 + pr * RP), 0, 4 * (p0 + sub) + fo, stage);
         bulk_commit();
       }
     }
   }
-  if (threadIdx.x == 0) bulk_wait0();
+  if (issuer) bulk_wait0();
   tmem_fence_before_sync();
   __syncthreads();
   if (warp == 0) {
