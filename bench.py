@@ -355,13 +355,15 @@ def run_ours(args, ws, rank, local):
     # ---- end to end through the public drop-in API, host numpy in/out
     e2e = None
     if not args.no_e2e:
+        # the caller's setup objects, built once as a user of the reference API does
+        quad, spec = case.quadrature, pk.PropagatorSpec.exact()
         for _ in range(3):  # warm-up: contexts, phase table, pinned buffers in rotation
-            out = pk.averaged_tendency(case.state, case.quadrature, case.params, pk.PropagatorSpec.exact())
+            out = pk.averaged_tendency(case.state, quad, case.params, spec)
         torch.cuda.synchronize()
         barrier(ws)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            out = pk.averaged_tendency(case.state, case.quadrature, case.params, pk.PropagatorSpec.exact())
+            out = pk.averaged_tendency(case.state, quad, case.params, spec)
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
         e2e = {"value": ws * P * case.dof * args.e2e_steps / e2e_s, "unit": UNIT,
