@@ -238,6 +238,20 @@ def load_traffic(n, kernel, phases_per_launch):
     return None
 
 
+def load_pipes(n, kernel):
+    """fp64-pipe and shared-memory-wavefront utilisation of `kernel` from the
+    latest committed ncu summary (the bounds that actually bind; HBM does not)."""
+    for path in sorted((ROOT / "profiles").glob("ncu_summary_r*.json"), reverse=True):
+        try:
+            ent = json.loads(path.read_text()).get(kernel, {}).get(str(n))
+        except (OSError, ValueError):
+            continue
+        if isinstance(ent, dict) and "fp64_pipe_frac" in ent:
+            return {"fp64_pipe_frac": ent["fp64_pipe_frac"], "smem_wavefront_frac": ent["smem_wavefront_frac"],
+                    "source": path.name}
+    return None
+
+
 def fp64_roofline(n, P, ms_per_step, sm_clock_ghz=1.965):
     """The fp64 side of the bound: the evaluation's DP thread-instruction count
     (per-phase ncu counts of the committed profile summary x P) against the
@@ -345,7 +359,7 @@ def run_ours(args, ws, rank, local):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak["value"],
                 "unit": "GB/s", "frac": achieved / peak["value"], "peak_source": peak["source"],
                 "traffic": traffic, "alg_bytes_per_launch": dom_bytes,
-                "launch_ms": per_launch_ms}
+                "launch_ms": per_launch_ms, "pipes": load_pipes(n, dom)}
     fp64 = fp64_roofline(n, P, ms_per_step)
     rhs_achieved = ab["B_eval"] / (ms_per_step * 1e-3) / 1e9
     rhs_roofline = {"bound": "hbm", "B_eval": ab["B_eval"], "achieved": rhs_achieved,

@@ -22,6 +22,9 @@ for d in data:
     res[k] = {"512": {"bytes_per_launch": dram, "phases_per_launch": phases, "bytes_per_phase": dram / phases,
                       "duration_us": float(d[ix["gpu__time_duration.sum"]]),
                       "dp_thread_instr_per_phase": sum(op.values()) * cyc / phases,
-                      "dp_flop_per_phase": (op["dadd"] + op["dmul"] + 2 * op["dfma"]) * cyc / phases}}
+                      "dp_flop_per_phase": (op["dadd"] + op["dmul"] + 2 * op["dfma"]) * cyc / phases,
+                      # pipe utilisation of this (serialised, cold-cache) launch
+                      "fp64_pipe_frac": float(d[ix["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]]) / 100,
+                      "smem_wavefront_frac": float(d[ix["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]]) / 100}}
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps({k: v for k, v in res.items() if k.startswith("pass")}, indent=1))
