@@ -246,7 +246,7 @@ int launchB(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, 
 template <int NX>
 int pass_c_groups(const pswe_ctx* c, int CP) {
   // phase groups per chunk: the grid (cols x Gc CTAs) should fill whole waves
-  // of the 3 x 148 resident CTAs, each CTA keeping >= 4 phases to amortise its
+  // of the resident CTAs (occupancy query), each CTA keeping >= 4 phases to amortise its
   // prologue and slot update.  Pick the Gc with the best wave efficiency.
   const int cols = (c->Ky + PassCW<NX>::GPW - 1) / PassCW<NX>::GPW;
   int per_sm = 0;

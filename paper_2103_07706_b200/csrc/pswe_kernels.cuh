@@ -12,9 +12,10 @@
 //             j = 0..KYM (spectral y), x = 0..nx-1 (physical x): each pass-A
 //             transform stores one contiguous column.
 //   I2 (pass B -> C): I2[p][f][j][x], f in 0..3: one ky column contiguous
-//             for pass C's bulk copies.  A pass-B CTA stages the outputs of
-//             its R consecutive rows as a [f][j][R] tile in shared memory
-//             and writes it with one TMA tensor store (R x 16-byte runs).
+//             for pass C's bulk copies.  A pair of pass-B warps stages the
+//             outputs of its RP consecutive rows as a [f][j][RP] tile in
+//             shared memory and writes it with one TMA tensor store
+//             (RP x 16-byte runs: full 32-byte sectors at 512^2).
 //   Pass A stores are contiguous; pass B reads its rows of I1 with TMA
 //   tensor gathers (one box = one row, 16-byte elements) issued a transform
 //   ahead.
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   }
 }
 
-// Unpack a forward pair transform (as unpack_store) into the CTA's staging
+// Unpack a forward pair transform (as unpack_store) into the warp pair's staging
 // tile [2 fields][Ky][R] at tile row rc, in the swizzled layout of the TMA
 // store map: a tile line (one field, one j: R complex = R * 16 bytes) has its
 // 16-byte chunks permuted, chunk' = chunk ^ ((line >> 1) & 3) for 64-byte
