@@ -63,3 +63,23 @@ def test_drop_in_call_matches_full_transfer():
     ref = dynamics.download(ctx.averaged_tendency(dynamics.upload(ctx, noisy)))
     for x, y in zip((got.u, got.v, got.eta), ref):
         assert np.array_equal(x, y)
+
+
+def test_drop_in_call_odd_host_arrays():
+    """Read-only, Fortran-ordered and negative-stride host fields give the
+    same result as plain C-contiguous ones (the staging copy handles them)."""
+    c = cases.case_c5(3, 4)
+    st = c.state
+    spec = pk.PropagatorSpec.exact()
+    ref = pk.averaged_tendency(st, c.quadrature, c.params, spec)
+    ro = [np.array(a) for a in (st.u, st.v, st.eta)]
+    for a in ro:
+        a.setflags(write=False)
+    fortran = [np.asfortranarray(a) for a in (st.u, st.v, st.eta)]
+    flipped = [np.flipud(np.flipud(a).copy()) for a in (st.u, st.v, st.eta)]  # negative strides
+    assert flipped[0].strides[0] < 0
+    for fields in (ro, fortran, flipped):
+        s2 = type(st)(grid=st.grid, u=fields[0], v=fields[1], eta=fields[2], t=st.t)
+        got = pk.averaged_tendency(s2, c.quadrature, c.params, spec)
+        for x, y in zip((got.u, got.v, got.eta), (ref.u, ref.v, ref.eta)):
+            assert np.array_equal(x, y)
