@@ -288,37 +288,7 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   return PSWE_OK;
 }
 
-template <int NX>
-int launchA2(pswe_ctx* c, int p0, int np, const double2* Uc, double2* I1, cudaStream_t st) {
-  using W = PassA2W<NX>;
-  const size_t smem = W::bytes();
-  auto kern = passA2_kernel<NX>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int cols = (c->Ky + W::GPW - 1) / W::GPW;
-  // phase groups of about 16 phases (the triplet set-up costs about one
-  // transform per warp and group)
-  const int ngrp = std::max(1, (np + 8) / 16);
-  const int gs = (np + ngrp - 1) / ngrp;
-  const int blocks = cols * ((np + gs - 1) / gs);
-  ProfScope ps(c, 0, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), p0, np, gs, Uc, c->ctab_cur, I1);
-  c->launches++;
-  CU(cudaGetLastError());
-  return PSWE_OK;
-}
-
 int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, cudaStream_t st) {
-  if (c->ctab_cur && !getenv("PSWE_PASSA_V1")) {
-    switch (c->nx) {
-      case 8: return launchA2<8>(c, p0, np, Uc, I1, st);
-      case 16: return launchA2<16>(c, p0, np, Uc, I1, st);
-      case 32: return launchA2<32>(c, p0, np, Uc, I1, st);
-      case 64: return launchA2<64>(c, p0, np, Uc, I1, st);
-      case 128: return launchA2<128>(c, p0, np, Uc, I1, st);
-      case 256: return launchA2<256>(c, p0, np, Uc, I1, st);
-      case 512: return launchA2<512>(c, p0, np, Uc, I1, st);
-    }
-  }
   switch (c->nx) {
     case 8: return launchA<8>(c, ph, p0, np, Uc, I1, st);
     case 16: return launchA<16>(c, ph, p0, np, Uc, I1, st);

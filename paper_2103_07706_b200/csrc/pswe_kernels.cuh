@@ -226,117 +226,6 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
   }
 }
 
-// ----------------------------------------------------------------------------
-// pass A, exact route with a phase table: register-resident exponential.
-// e^{sL}U = U + c1(s) LU + c2(s) L^2 U per mode, and U, LU, L^2 U do not
-// depend on the phase.  A CTA owns GPW ky columns (one per lane group) and a
-// group of consecutive phases; each warp computes the (X, LX, L^2X) triplet
-// of ONE field at the 2/3-band positions its lanes own in the type-1 input
-// layout, once, and keeps it in registers, so a phase costs two FMAs per
-// component plus the (c1, c2) loads -- no shared-memory stash, no CTA
-// barrier.  Warp roles (balanced at two transforms per two phases):
-//   0 / 1: u for the even / odd phases of the group (u', then ikx u')
-//   2 / 3: v likewise (v', ikx v')
-//   4    : depth eta' - b for every phase
-// The 1/(nx ny) normalisation is folded into the triplets.
-// ----------------------------------------------------------------------------
-template <int NX>
-struct PassA2W {
-  static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
-  static constexpr int WARPS = 5;
-  static constexpr int CTAS = 3;
-  static constexpr int Kx = 2 * (NX / 3) + 1;
-  // triplets [3 fields][X, LX, L2X][GPW][Kx] | xbuf per group
-  static size_t bytes() {
-    return (size_t)9 * GPW * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
-  }
-};
-
-// band class of register slot n1 (positions t + T n1, t = 0..T-1):
-// 0 all out of band, 1 all in band, 2 straddles a band edge
-template <int N>
-__host__ __device__ constexpr int slot_class(int n1) {
-  constexpr int T = WF<N>::T, K = N / 3;
-  const int kmin = T * n1, kmax = T * n1 + T - 1;
-  if (kmax <= K || kmin >= N - K) return 1;
-  if (kmin > K && kmax < N - K) return 0;
-  return 2;
-}
-
-template <int NX>
-__global__ void __launch_bounds__(PassA2W<NX>::WARPS * 32, PassA2W<NX>::CTAS)
-    passA2_kernel(GridDev G, int p0, int np, int gs, const double2* __restrict__ Uc,
-                  const double2* __restrict__ ctab, double2* __restrict__ I) {
-  using W = PassA2W<NX>;
-  constexpr int T = W::T, P = W::P, GPW = W::GPW;
-  constexpr int K = NX / 3, Kx = W::Kx;
-  constexpr int TS = GPW * Kx;  // one triplet component of the CTA's columns
-  extern __shared__ __align__(128) unsigned char sbytes[];
-  double2* trip = reinterpret_cast<double2*>(sbytes);
-  const int Ky = G.Ky;
-  const int cols = (Ky + GPW - 1) / GPW;
-  const int cb = blockIdx.x % cols, grp = blockIdx.x / cols;
-  const int pa = grp * gs, pb = min(np, pa + gs);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tl = lane / T, t = lane % T;
-  const int j = cb * GPW + tl;
-  const bool active = j < Ky;
-  const int jj = active ? j : Ky - 1;
-  double* xb = reinterpret_cast<double*>(trip + 9 * TS) + (size_t)(warp * GPW + tl) * WF<NX>::XBUF;
-  const WLane wl = wlane<NX>(G.twx, t);
-  const size_t KyKx = (size_t)Ky * Kx;
-
-  // the CTA's triplets, once: (X, LX, L^2X) / (nx ny) for X = u, v, eta - b
-  for (int idx = threadIdx.x; idx < TS; idx += blockDim.x) {
-    const int tt = idx / Kx, r = idx % Kx;
-    const int jc = min(cb * GPW + tt, Ky - 1);
-    const size_t o = (size_t)jc * Kx + r;
-    const C3 q = {__ldg(Uc + o), __ldg(Uc + KyKx + o), __ldg(Uc + 2 * KyKx + o)};
-    const double kx = __ldg(G.kxc + r), ky = __ldg(G.kyc + jc);
-    const C3 l1 = lin(q, G.ph, kx, ky);
-    const C3 l2 = lin(l1, G.ph, kx, ky);
-    const double sc = G.inv_n2;
-    trip[0 * TS + idx] = cscale(sc, q.u);
-    trip[1 * TS + idx] = cscale(sc, l1.u);
-    trip[2 * TS + idx] = cscale(sc, l2.u);
-    trip[3 * TS + idx] = cscale(sc, q.v);
-    trip[4 * TS + idx] = cscale(sc, l1.v);
-    trip[5 * TS + idx] = cscale(sc, l2.v);
-    trip[6 * TS + idx] = cscale(sc, csub(q.e, __ldg(G.bc + o)));
-    trip[7 * TS + idx] = cscale(sc, l1.e);
-    trip[8 * TS + idx] = cscale(sc, l2.e);
-  }
-  __syncthreads();
-
-  // role: field fld (0 u, 1 v, 2 depth), phase parity / stride
-  const int fld = warp < 4 ? (warp >> 1) : 2;
-  const int pstart = pa + (warp < 4 ? (warp & 1) : 0), pstep = warp < 4 ? 2 : 1;
-  const double2* tX = trip + (size_t)(3 * fld) * TS + (size_t)tl * Kx;
-#pragma unroll 1
-  for (int p = pstart; p < pb; p += pstep) {
-    const double2* ct = ctab + ((size_t)(p0 + p) * Ky + jj) * Kx;
-#pragma unroll 1
-    for (int d = 0; d < (fld < 2 ? 2 : 1); ++d) {
-      double2 v[P];
-#pragma unroll
-      for (int n1 = 0; n1 < P; ++n1) {
-        v[n1] = czero();
-        if (slot_class<NX>(n1) == 0) continue;
-        const int r = band_r(t + T * n1, NX, K, Kx);
-        if (slot_class<NX>(n1) == 2 && r < 0) continue;
-        const double2 c = __ldg(ct + r);
-        const double2 x0 = tX[r], x1 = tX[TS + r], x2 = tX[2 * TS + r];
-        double2 e = cmk(fma(c.y, x2.x, fma(c.x, x1.x, x0.x)), fma(c.y, x2.y, fma(c.x, x1.y, x0.y)));
-        if (d) e = cik(__ldg(G.kxc + r), e);
-        v[n1] = e;
-      }
-      wfft_t1<NX, true, true>(v, t, xb, wl);
-      const int fo = d ? 3 + fld : fld;
-      if (active) store_t1_strided<NX>(v, t, I + (((size_t)p * 5 + fo) * Ky + j) * NX, 1);
-    }
-  }
-}
-
 // ============================================================================
 // pass B: per physical row x: y-C2R of the 7 fields (paired by physical
 // dimension: (u,v), (ux,uy), (vx,vy), (depth,0)), quadratic products, y-R2C
