@@ -326,6 +326,18 @@ def run_ours(args, ws, rank, local):
     units = ws * P * case.dof * args.steps
     value = units / (dev_ms * 1e-3)
 
+    # ---- N > 1: the phase-sharded (strong-scaling) evaluation beside the
+    # replicas: each rank takes a contiguous slice of the live phases, then
+    # one NCCL all-gather of the compact partial sums and a rank-ordered sum
+    # (sharding.py).  Extra information; `value` stays the replicas' number.
+    sharded = None
+    if ws > 1:
+        try:
+            sharded = run_sharded(args, ws, rank, ctx, case, Uc, Ac, flush, stream, dev, ms_per_step)
+        except Exception as exc:  # never lose the contract line to the extra measurement
+            sharded = {"error": f"{type(exc).__name__}: {exc}"}
+        ctx.set_quadrature(case.quadrature.s, case.quadrature.w)
+
     # ---- per-kernel split (CUDA events around each launch, separate pass).
     # One chunk lane here: with overlapping lanes an event pair would also
     # time the other lanes' kernels; serialised, the shares are comparable
@@ -409,10 +421,37 @@ def run_ours(args, ws, rank, local):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "gpu": torch.cuda.get_device_name(local), "sweep": sweep, "step_configs": steps_info,
         }
+        if sharded is not None:
+            line["phase_sharded"] = sharded
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def run_sharded(args, ws, rank, ctx, case, Uc, Ac, flush, stream, dev, one_rank_ms):
+    """One averaged RHS split over the ranks by phase (device time, max over ranks)."""
+    import torch
+    from paper_2103_07706_b200.sharding import ordered_gather_sum, shard_weights
+
+    ctx.set_quadrature(case.quadrature.s, shard_weights(case.quadrature.w, ws, rank))
+    for _ in range(args.warmup):
+        ordered_gather_sum(ctx.averaged_tendency_compact(Uc, Ac))
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = 0.0
+    for _ in range(args.steps):
+        flush_l2(flush)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ordered_gather_sum(ctx.averaged_tendency_compact(Uc, Ac))
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    ms = max_over_ranks(ms, ws, dev) / args.steps
+    return {"ms_per_step": ms, "value": case.P * case.dof / (ms * 1e-3), "unit": UNIT,
+            "speedup_vs_one_gpu": one_rank_ms / ms, "scaling": "strong",
+            "collective": "NCCL all_gather of the compact 2/3-band partial sums, rank-ordered sum"}
 
 
 def run_step_configs(pk, cases, torch, stream):
