@@ -235,10 +235,20 @@ int launchB_pair(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap&
   return PSWE_OK;
 }
 
+// The phase-paired kernel runs 11 row transforms in sequence per warp, the
+// single-phase one 6: when the pair grids of all lanes together would not
+// even give every SM one CTA (small grids, few phases), the evaluation is
+// latency-bound and the shorter chain wins (64^2, M = 8: 54 -> 44 us per
+// RHS; the C2 step 178 -> 129 us); with more CTAs the pair kernel's
+// efficiency wins (256^2, M = 8, 256 pair CTAs: 64 vs 67 us).
 template <int NY>
-int launchB(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2, cudaStream_t st) {
+int launchB(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2,
+            cudaStream_t st) {
   if constexpr (NY >= 64) {
-    if (passB_fast(c)) return launchB_pair<NY>(c, np, mI1, mO, st);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const long long pair_ctas = (long long)lanes * ((np + 1) / 2) * c->nx / PassBW<NY>::GPC;
+    if (passB_fast(c) && pair_ctas >= sms + sms / 3) return launchB_pair<NY>(c, np, mI1, mO, st);
   }
   return launchB_small<NY>(c, np, mI1, I2, st);
 }
@@ -259,7 +269,10 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
   const int slots = per_sm * sms;
   int best = 1;
   double best_eff = 0.0;
-  for (int g = 1; g <= std::max(1, CP / 4) && g <= 16; ++g) {
+  // a grid that cannot fill the SMs even at 4 phases per CTA is latency-
+  // bound: then down to one phase per CTA (64^2, M = 8: pass C 16 -> 9 us)
+  const int gmax = (long long)cols * std::max(1, CP / 4) < sms ? CP : std::max(1, CP / 4);
+  for (int g = 1; g <= gmax && g <= 16; ++g) {
     const int ctas = cols * g;
     const int waves = (ctas + slots - 1) / slots;
     const double eff = (double)ctas / ((double)waves * slots);
@@ -300,15 +313,16 @@ int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
-int dispatchB(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2, cudaStream_t st) {
+int dispatchB(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2,
+              cudaStream_t st) {
   switch (c->ny) {
-    case 8: return launchB<8>(c, np, mI1, mO, I2, st);
-    case 16: return launchB<16>(c, np, mI1, mO, I2, st);
-    case 32: return launchB<32>(c, np, mI1, mO, I2, st);
-    case 64: return launchB<64>(c, np, mI1, mO, I2, st);
-    case 128: return launchB<128>(c, np, mI1, mO, I2, st);
-    case 256: return launchB<256>(c, np, mI1, mO, I2, st);
-    case 512: return launchB<512>(c, np, mI1, mO, I2, st);
+    case 8: return launchB<8>(c, np, lanes, mI1, mO, I2, st);
+    case 16: return launchB<16>(c, np, lanes, mI1, mO, I2, st);
+    case 32: return launchB<32>(c, np, lanes, mI1, mO, I2, st);
+    case 64: return launchB<64>(c, np, lanes, mI1, mO, I2, st);
+    case 128: return launchB<128>(c, np, lanes, mI1, mO, I2, st);
+    case 256: return launchB<256>(c, np, lanes, mI1, mO, I2, st);
+    case 512: return launchB<512>(c, np, lanes, mI1, mO, I2, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported ny = %d", c->ny);
 }
@@ -467,7 +481,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     double2* I2 = I1 + (size_t)5 * c->Ky * c->nx * CP;
     double2* sl = c->slots.p + (size_t)L * Gc * c->compact_elems();
     TRY(dispatchA(c, ph, p0, np, Uc, I1, lst[L]));
-    TRY(dispatchB(c, np, mrow[L], mcol[L], I2, lst[L]));
+    TRY(dispatchB(c, np, lanes, mrow[L], mcol[L], I2, lst[L]));
     TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
   }
   for (int L = 1; L < lanes; ++L) {
