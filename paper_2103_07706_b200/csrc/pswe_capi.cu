@@ -192,8 +192,10 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
   const size_t smem = W::bytes(c->Kx);
   auto kern = passA_kernel<NX>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int nblk = np * ((c->Ky + W::GPW - 1) / W::GPW);
-  const int blocks = std::min(nblk, 4 * 148);
+  const int nblk = ((np + 1) / 2) * ((c->Ky + W::GPW - 1) / W::GPW);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int blocks = std::min(nblk, W::CTAS * sms);
   ProfScope ps(c, 0, st);
   kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, I1);
   c->launches++;

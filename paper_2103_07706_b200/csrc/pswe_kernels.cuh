@@ -118,21 +118,26 @@ template <int NX>
 struct PassAW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 5;
-  // mbarrier | buffer [5][GPW][Kx] (u, v, eta, b, (c1,c2) -> u', v', depth in place) | xbuf per group | kx [Kx]
+  // 3 CTAs/SM (no spills for nx >= 32); at 4 CTAs/SM (96 registers) the
+  // phase-pair block spills and measured slower
+  static constexpr int CTAS = 3;
+  // mbarrier | buffer [6][GPW][Kx] (u, v, eta, b, (c1,c2)_p, (c1,c2)_q ->
+  // u'_p, v'_p, depth_p, u'_q, v'_q, depth_q in place) | xbuf per group
   static size_t bytes(int Kx) {
-    return 16 + (size_t)GPW * 5 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) +
-           (size_t)Kx * sizeof(double);
+    return 16 + (size_t)GPW * 6 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
   }
 };
 
 // Persistent CTAs over "task blocks" (GPW consecutive ky columns of one
-// phase).  Per block: the compact U columns, b and the phase table's
-// (c1, c2) are TMA-bulk-prefetched (one buffer, refilled as soon as the FFT
-// inputs are in registers), the whole CTA applies e^{sL} per mode in place,
-// then warp f runs the inverse x-FFT of output field f (u, v, eta-b, ikx u,
-// ikx v) for the block's GPW columns and stores it to I1.
+// phase PAIR p, q = p + 1).  Per block: the compact U columns, b and the
+// phase table's (c1, c2) columns of both phases are TMA-bulk-prefetched
+// (one buffer, refilled as soon as the FFT inputs are in registers), the
+// whole CTA applies e^{s_p L} and e^{s_q L} per mode in place (U is read once
+// for both phases), then warp f runs the inverse x-FFTs of output field f
+// (u, v, eta-b, ikx u, ikx v) of both phases and stores them to I1.  Two CTA
+// barriers per two transforms per warp.
 template <int NX>
-__global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
+__global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
     passA_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, const double2* __restrict__ Uc,
                  const double2* __restrict__ ctab, double2* __restrict__ I) {
   using W = PassAW<NX>;
@@ -141,27 +146,28 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
   constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
   const int Ky = G.Ky;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
-  double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [5][GPW][Kx]
-  double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * 5 * Kx);
-  double* kxs = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;
+  double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [6][GPW][Kx]
+  double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * 6 * Kx);
   const bool tab = ctab != nullptr;
   const int cols = (Ky + GPW - 1) / GPW;
-  const int nblk = np * cols;
+  const int npair = (np + 1) / 2;
+  const int nblk = npair * cols;
   const size_t KyKx = (size_t)Ky * Kx, fs = (size_t)GPW * Kx;
   const int lane = threadIdx.x & 31, f = threadIdx.x >> 5;  // warp = output field
-  for (int i = threadIdx.x; i < Kx; i += blockDim.x) kxs[i] = G.kxc[i];
 
-  // block -> (phase pl, first column j0, ncol columns): contiguous in U, b, ctab.
-  // Warp 0: lane 0 posts the byte count, lanes 0..4 each issue one bulk copy.
+  // block -> (phase pair pp, first column j0, ncol columns): contiguous in U, b, ctab.
+  // Warp 0: lane 0 posts the byte count, lanes 0..5 each issue one bulk copy.
   auto prefetch = [&](int blk) {
-    const int pl = blk / cols, j0 = (blk % cols) * GPW;
+    const int pp = blk / cols, j0 = (blk % cols) * GPW;
     const int ncol = min(GPW, Ky - j0);
+    const int nq = (2 * pp + 1 < np) ? 2 : 1;
     const uint32_t seg = (uint32_t)(ncol * Kx * sizeof(double2));
-    if (lane == 0) mbar_arrive_expect_tx(bar, (tab ? 5 : 4) * seg);
+    if (lane == 0) mbar_arrive_expect_tx(bar, (tab ? 4 + nq : 4) * seg);
     __syncwarp();
     if (lane < 3) bulk_g2s(buf + lane * fs, Uc + lane * KyKx + (size_t)j0 * Kx, seg, bar);
     if (lane == 3) bulk_g2s(buf + 3 * fs, G.bc + (size_t)j0 * Kx, seg, bar);
-    if (lane == 4 && tab) bulk_g2s(buf + 4 * fs, ctab + (size_t)(p0 + pl) * KyKx + (size_t)j0 * Kx, seg, bar);
+    if (tab && lane >= 4 && lane - 4 < nq)
+      bulk_g2s(buf + lane * fs, ctab + (size_t)(p0 + 2 * pp + lane - 4) * KyKx + (size_t)j0 * Kx, seg, bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
@@ -173,56 +179,70 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, 4)
   const int tl = lane / T, t = lane % T;
   double* xb = xbuf + (size_t)(f * GPW + tl) * WF<NX>::XBUF;
   const WLane wl = wlane<NX>(G.twx, t);
-  // one loop-carried counter (blk derived from it): a second one was spilled
-  // and its reload queued behind the column stores
+  const int fi = f < 3 ? f : f - 3;  // source slot of this warp's field
 #pragma unroll 1
   for (int it = 0;; ++it) {
     const int blk = (int)blockIdx.x + it * (int)gridDim.x;
     if (blk >= nblk) break;
-    const int pl = blk / cols, j0 = (blk % cols) * GPW;
+    const int pp = blk / cols, j0 = (blk % cols) * GPW;
     const int ncol = min(GPW, Ky - j0);
-    const double s = tab ? 0.0 : ph.s[p0 + pl];  // the exact route never reads it
+    const int pa = 2 * pp;
+    const bool hasq = pa + 1 < np;
     mbar_wait(bar, it & 1);
-    // e^{sL} per mode in place: (u, v, eta, b) -> (u', v', eta' - b) / (nx ny)
+    // e^{sL} per mode for both phases, in place:
+    // (u, v, eta, b, c_p, c_q) -> (u', v', eta' - b)_p, (u', v', eta' - b)_q, / (nx ny)
     double kyb[GPW];
 #pragma unroll
     for (int c = 0; c < GPW; ++c) kyb[c] = G.kyc[min(j0 + c, Ky - 1)];
     for (int idx = threadIdx.x; idx < ncol * Kx; idx += blockDim.x) {
       const int tt = idx / Kx, r = idx % Kx;
       double2* e = buf + idx;
-      C3 q = {e[0], e[fs], e[2 * fs]};
-      const double kx = kxs[r];
+      const C3 q0 = {e[0], e[fs], e[2 * fs]};
+      const double2 bb = e[3 * fs];
+      const double kx = __ldg(G.kxc + r);
       double ky = kyb[0];
 #pragma unroll
       for (int c = 1; c < GPW; ++c)
         if (tt == c) ky = kyb[c];
-      if (tab)
-        q = exp_c12(e[4 * fs], q, G.ph, kx, ky);
-      else
-        q = expL(s, q, G.ph, kx, ky, pr);
-      // slots 0..2 become u', v', eta' - b (the ikx fields are formed by the
-      // consuming warps; writing them into slots 3/4 here raced with the
-      // next block's TMA refill of those slots in testing)
-      e[0] = cscale(G.inv_n2, q.u);
-      e[fs] = cscale(G.inv_n2, q.v);
-      e[2 * fs] = cscale(G.inv_n2, csub(q.e, e[3 * fs]));
+      const double2 cb = (tab && hasq) ? e[5 * fs] : czero();
+#pragma unroll 1
+      for (int sub = 0; sub < (hasq ? 2 : 1); ++sub) {
+        C3 q = tab ? exp_c12(sub ? cb : e[4 * fs], q0, G.ph, kx, ky)
+                   : expL(ph.s[p0 + pa + sub], q0, G.ph, kx, ky, pr);
+        double2* o = e + (size_t)(3 * sub) * fs;
+        o[0] = cscale(G.inv_n2, q.u);
+        o[fs] = cscale(G.inv_n2, q.v);
+        o[2 * fs] = cscale(G.inv_n2, csub(q.e, bb));
+      }
     }
     fence_proxy_async();  // order these stores before the next block's TMA refill of buf
     __syncthreads();
     const bool active = tl < ncol;
-    double2 v[P];
-    band_gather<NX>(v, t, buf + (size_t)(f < 3 ? f : f - 3) * fs + (size_t)tl * Kx, active);
-    if (f >= 3) {  // ikx u', ikx v'
-#pragma unroll
-      for (int n1 = 0; n1 < P; ++n1) {
-        const int r = band_r(t + T * n1, NX, NX / 3, Kx);
-        if (r >= 0) v[n1] = cik(kxs[r], v[n1]);
+#define PSWE_A_GATHER(v, sub)                                                         \
+  band_gather<NX>(v, t, buf + (size_t)(fi + 3 * (sub)) * fs + (size_t)tl * Kx, active);  \
+  if (f >= 3) { /* ikx u', ikx v' */                                                 \
+    _Pragma("unroll") for (int n1 = 0; n1 < P; ++n1) {                                 \
+      const int r = band_r(t + T * n1, NX, NX / 3, Kx);                                \
+      if (r >= 0) v[n1] = cik(__ldg(G.kxc + r), v[n1]);                                \
+    }                                                                                  \
+  }
+    double2* const out0 = I + ((((size_t)pa) * 5 + f) * Ky + j0 + tl) * NX;
+    double2* const out1 = out0 + (size_t)5 * Ky * NX;
+    // both phases through one copy of the transform code; the buffer is
+    // released (and refilled for the next block) after the last gather
+    const int nsub = hasq ? 2 : 1;
+#pragma unroll 1
+    for (int sub = 0; sub < nsub; ++sub) {
+      double2 v[P];
+      PSWE_A_GATHER(v, sub)
+      if (sub == nsub - 1) {
+        __syncthreads();  // buffer consumed: refill it for the next block while the FFT runs
+        if (f == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
       }
+      wfft_t1<NX, true, true>(v, t, xb, wl);
+      if (active) store_t1_strided<NX>(v, t, sub ? out1 : out0, 1);
     }
-    __syncthreads();  // buffer consumed: refill it for the next block while the FFTs run
-    if (f == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
-    wfft_t1<NX, true, true>(v, t, xb, wl);
-    if (active) store_t1_strided<NX>(v, t, I + (((size_t)pl * 5 + f) * Ky + j0 + tl) * NX, 1);
+#undef PSWE_A_GATHER
   }
 }
 
