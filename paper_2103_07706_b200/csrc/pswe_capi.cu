@@ -475,13 +475,16 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     CU(cudaEventRecord(c->ev_fork, st));
     for (int L = 1; L < lanes; ++L) CU(cudaStreamWaitEvent(lst[L], c->ev_fork, 0));
   }
+  const bool direct = nchunks == 1 && Gc == 1;
   int chunk = 0;
   for (int p0 = 0; p0 < P; p0 += CP, ++chunk) {
     const int np = std::min(CP, P - p0);
     const int L = chunk % lanes;
     double2* I1 = c->inter.p + (size_t)L * per_phase * CP;
     double2* I2 = I1 + (size_t)5 * c->Ky * c->nx * CP;
-    double2* sl = c->slots.p + (size_t)L * Gc * c->compact_elems();
+    // a single slot (one chunk, Gc = 1, e.g. the fine-step reference's one
+    // node) is the output itself: pass C writes it, no reduction launch
+    double2* sl = direct ? Ac : c->slots.p + (size_t)L * Gc * c->compact_elems();
     TRY(dispatchA(c, ph, p0, np, Uc, I1, lst[L]));
     TRY(dispatchB(c, np, lanes, mrow[L], mcol[L], I2, lst[L]));
     TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
@@ -490,6 +493,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     CU(cudaEventRecord(c->ev_lane[L - 1], lst[L]));
     CU(cudaStreamWaitEvent(st, c->ev_lane[L - 1], 0));
   }
+  if (direct) return PSWE_OK;
   const size_t n = c->compact_elems();
   ProfScope ps(c, 3, st);
   reduce_slots_kernel<<<elem_grid(n), 256, 0, st>>>(c->slots.p, lanes * Gc, n, Ac);
