@@ -223,6 +223,20 @@ int launchB_small(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cuda
 }
 
 template <int NY>
+int launchB_split(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cudaStream_t st) {
+  using W = PassBSW<NY>;
+  const size_t smem = W::bytes();
+  auto kern = passB_split_kernel<NY>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int blocks = (np * c->nx + W::GPW - 1) / W::GPW;
+  ProfScope ps(c, 1, st);
+  kern<<<blocks, 128, smem, st>>>(c->grid(), np, mI1, I2);
+  c->launches++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+template <int NY>
 int launchB_pair(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, cudaStream_t st) {
   using W = PassBW<NY>;
   const size_t smem = W::template bytes<true>();
@@ -251,6 +265,14 @@ int launchB(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUtens
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const long long pair_ctas = (long long)lanes * ((np + 1) / 2) * c->nx / PassBW<NY>::GPC;
     if (passB_fast(c) && pair_ctas >= sms + sms / 3) return launchB_pair<NY>(c, np, mI1, mO, st);
+  }
+  // fewer single-phase CTAs than SMs: split each row group's transforms over
+  // four warps (passB_split_kernel, two transform latencies instead of six)
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const long long small_ctas = (long long)lanes * ((np * c->nx + PassBW<NY>::GPC - 1) / PassBW<NY>::GPC);
+    if (small_ctas < sms && !getenv("PSWE_NO_SPLIT")) return launchB_split<NY>(c, np, mI1, I2, st);
   }
   return launchB_small<NY>(c, np, mI1, I2, st);
 }

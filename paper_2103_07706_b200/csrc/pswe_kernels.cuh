@@ -498,6 +498,85 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   }
 }
 
+// Latency-bound small grids (NY <= 64, few rows in flight): the four
+// inverse transforms of a row group run on four warps at once instead of in
+// sequence -- warp w: 0 (u, v), 1 (ux, i ky u), 2 (vx, i ky v), 3 (depth) --
+// the physical values meet in shared memory, and warps 0 and 1 run the two
+// forward transforms (A + iB, C + iD) side by side: two transform latencies
+// per row group instead of six.  Same inputs, outputs and arithmetic per
+// value as passB_kernel.
+template <int NY>
+struct PassBSW {
+  static constexpr int T = WF<NY>::T, P = WF<NY>::P, GPW = WF<NY>::GPW;
+  static constexpr int KYA = PassBW<NY>::KYA;
+  // per warp: prefetch [GPW][2][KYA] | xbuf per group | mbarrier; then the
+  // physical stash [4][P][32] | ky [Ky]
+  static constexpr size_t WB =
+      ((size_t)GPW * 2 * KYA * sizeof(double2) + (size_t)GPW * WF<NY>::XBUF * sizeof(double) + 8 + 127) / 128 * 128;
+  static size_t bytes() {
+    return 4 * WB + (size_t)4 * P * 32 * sizeof(double2) + (size_t)PassBW<NY>::Ky * sizeof(double) + 16;
+  }
+};
+
+template <int NY>
+__global__ void __launch_bounds__(128)
+    passB_split_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, double2* __restrict__ I2) {
+  using W = PassBSW<NY>;
+  constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA;
+  constexpr int Ky = PassBW<NY>::Ky;
+  extern __shared__ __align__(128) unsigned char sbytes[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane % T, g = lane / T;
+  unsigned char* wbase = sbytes + (size_t)warp * W::WB;
+  double2* pre = reinterpret_cast<double2*>(wbase);
+  double* xb = reinterpret_cast<double*>(pre + (size_t)GPW * 2 * KYA) + (size_t)g * WF<NY>::XBUF;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + W::WB - 8);
+  double2* stash = reinterpret_cast<double2*>(sbytes + 4 * W::WB);  // [4][P][32]
+  double* kys = reinterpret_cast<double*>(stash + (size_t)4 * P * 32);
+  const int ntask = np * Gd.nx;
+  const int first_task = blockIdx.x * GPW;  // the CTA's row group, shared by its 4 warps
+  const int task = first_task + g;
+  const bool active = task < ntask;
+  const int pl = active ? task / Gd.nx : 0, x = active ? task % Gd.nx : 0;
+  const size_t KyNX = (size_t)Ky * Gd.nx;
+  double2* out = I2 + (size_t)pl * 4 * KyNX + x;
+  for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  passB_prefetch<NY>(warp, lane, pre, bar, &mI, first_task, ntask, Gd.nx);
+  const WLane wl = wlane<NY>(Gd.twy, t);
+  double2 v[P];
+  mbar_wait(bar, 0);
+  build_pair<NY>(v, t, pre + (size_t)g * 2 * KYA, kys, warp);
+  wfft_t1<NY, true, true>(v, t, xb, wl);
+  double2* mine = stash + (size_t)warp * P * 32;
+#pragma unroll
+  for (int i = 0; i < P; ++i) mine[i * 32 + lane] = v[i];
+  __syncthreads();
+  if (warp >= 2) return;
+  const double2* suv = stash;                 // (u, v)
+  const double2* sux = stash + P * 32;        // (ux, uy)
+  const double2* svx = stash + 2 * P * 32;    // (vx, vy)
+  const double2* sd = stash + 3 * P * 32;     // (depth, -)
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    const double2 q = suv[i * 32 + lane];
+    if (warp == 0) {
+      const double2 a = sux[i * 32 + lane], b = svx[i * 32 + lane];
+      v[i] = cmk(-(q.x * a.x + q.y * a.y), -(q.x * b.x + q.y * b.y));  // A + iB
+    } else {
+      const double d = sd[i * 32 + lane].x;
+      v[i] = cmk(q.x * d, q.y * d);  // C + iD = u depth + i v depth
+    }
+  }
+  wfft_t2<NY, false>(v, t, xb, wl);
+  const int fo = warp == 0 ? 0 : 2;
+  unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
+}
+
 // Unpack a forward pair transform (as unpack_store) into the warp pair's staging
 // tile [2 fields][Ky][R] at tile row rc, in the swizzled layout of the TMA
 // store map: a tile line (one field, one j: R complex = R * 16 bytes) has its
