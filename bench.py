@@ -383,7 +383,7 @@ def run_ours(args, ws, rank, local):
     if not args.no_e2e:
         # the caller's setup objects, built once as a user of the reference API does
         quad, spec = case.quadrature, pk.PropagatorSpec.exact()
-        for _ in range(3):  # warm-up: contexts, phase table, pinned buffers in rotation
+        for _ in range(5):  # warm-up: contexts, phase table, pinned buffers in rotation
             out = pk.averaged_tendency(case.state, quad, case.params, spec)
         torch.cuda.synchronize()
         barrier(ws)
@@ -564,7 +564,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--level", type=int, default=7)
     ap.add_argument("--M", type=int, default=256)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
