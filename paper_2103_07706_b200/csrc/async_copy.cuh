@@ -87,6 +87,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Order this thread's generic-proxy shared-memory writes before later
 // async-proxy (TMA) accesses of the same bytes: required before a bulk copy
 // overwrites a buffer the CTA has written with ordinary stores.
+// Programmatic dependent launch: wait for the preceding grid in the stream
+// (a no-op unless this grid was launched with programmatic stream
+// serialisation), and let the next grid be scheduled early.  Every kernel
+// of the RHS chain waits before its first global access, so only launch
+// latency and CTA scheduling overlap the predecessor.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

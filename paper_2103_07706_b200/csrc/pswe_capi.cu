@@ -128,6 +128,7 @@ struct pswe_ctx {
   int64_t launches = 0;
   // per-kernel event profiling
   bool prof = false;
+  bool pdl = false;  // programmatic dependent launch for the current chain (latency_bound)
   std::vector<cudaEvent_t> ev_pool;
   struct Rec { int cls; cudaEvent_t a, b; };
   std::vector<Rec> recs;
@@ -185,6 +186,34 @@ struct ProfScope {
   }
 };
 
+// Kernel launch, with programmatic stream serialisation when `pdl`: the
+// grid may be scheduled while its predecessor in the stream finishes (every
+// kernel of the chain waits on griddepcontrol before its first global
+// access).  Used for latency-bound evaluations only, where all CTAs of a
+// kernel fit in one wave: with several waves, early-scheduled CTAs of the
+// next kernel would take the slots of the current one's later waves.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// small grids: the RHS chain is launch- and latency-bound
+bool latency_bound(const pswe_ctx* c) {
+  static const bool off = getenv("PSWE_NO_PDL") != nullptr;
+  return !off && (size_t)c->nx * c->ny <= (size_t)128 * 128;
+}
+
 // ---------------------------------------------------------------- dispatch
 template <int NX>
 int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, cudaStream_t st) {
@@ -197,7 +226,7 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   const int blocks = std::min(nblk, W::CTAS * sms);
   ProfScope ps(c, 0, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, I1);
+  CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, I1));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -216,7 +245,7 @@ int launchB_small(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cuda
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, mI1, I2);
+  CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), np, mI1, I2));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -230,7 +259,7 @@ int launchB_split(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cuda
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = (np * c->nx + W::GPW - 1) / W::GPW;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, 128, smem, st>>>(c->grid(), np, mI1, I2);
+  CU(launch_k(c->pdl, kern, blocks, 128, smem, st, c->grid(), np, mI1, I2));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -245,7 +274,7 @@ int launchB_pair(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap&
   const int ntp = ((np + 1) / 2) * c->nx;
   const int blocks = (ntp + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), np, mI1, mO);
+  CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), np, mI1, mO));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -319,7 +348,8 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   const int cols = (c->Ky + W::GPW - 1) / W::GPW;
   const int blocks = cols * Gc;
   ProfScope ps(c, 2, st);
-  kern<<<blocks, W::WARPS * 32, smem, st>>>(c->grid(), c->prop(), ph, p0, np, Gc, I2, c->ctab_cur, slots, first);
+  CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), c->prop(), ph, p0, np, Gc, I2, c->ctab_cur,
+              slots, first));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -480,6 +510,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   const int CP = std::max(1, std::min(P, (P + nchunks - 1) / nchunks));
   nchunks = (P + CP - 1) / CP;
   const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
+  c->pdl = latency_bound(c) && nchunks == 1;
   TRY(c->inter.alloc(per_phase * CP * lanes));
   TRY(c->slots.alloc((size_t)lanes * Gc * c->compact_elems()));
   if (getenv("PSWE_DEBUG_POISON")) {  // debug: NaN-fill intermediates to expose unwritten entries
@@ -518,7 +549,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   if (direct) return PSWE_OK;
   const size_t n = c->compact_elems();
   ProfScope ps(c, 3, st);
-  reduce_slots_kernel<<<elem_grid(n), 256, 0, st>>>(c->slots.p, lanes * Gc, n, Ac);
+  CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(n), 256, 0, st, (const double2*)c->slots.p, lanes * Gc, n, Ac));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -573,22 +604,32 @@ int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
   const int P = (int)c->s_live.size();
   const int gb = elem_grid(n);
   // stage 1
-  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, U.u, U.v, U.e, c->Uc.p);
+  c->pdl = latency_bound(c);
+  CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, U.u, U.v, U.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
-  stage1_kernel<<<gb, 256, 0, st>>>(G, pr, dt, U, c->Ac.p, edt, u1, c->flags.p);
+  c->pdl = latency_bound(c);
+  CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)c->Ac.p, edt, u1, c->flags.p));
   c->launches++;
   // stage 2
-  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, u1.u, u1.v, u1.e, c->Uc.p);
+  c->pdl = latency_bound(c);
+  CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, (const double2*)u1.u,
+              (const double2*)u1.v, (const double2*)u1.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
-  stage2_kernel<<<gb, 256, 0, st>>>(G, pr, dt, U, f3c(u1), c->Ac.p, u2, c->flags.p);
+  c->pdl = latency_bound(c);
+  CU(launch_k(c->pdl, stage2_kernel, gb, 256, 0, st, G, pr, dt, U, f3c(u1), (const double2*)c->Ac.p, u2,
+              c->flags.p));
   c->launches++;
   // stage 3
-  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, u2.u, u2.v, u2.e, c->Uc.p);
+  c->pdl = latency_bound(c);
+  CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, (const double2*)u2.u,
+              (const double2*)u2.v, (const double2*)u2.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
-  stage3_kernel<<<gb, 256, 0, st>>>(G, pr, dt, f3c(edt), f3c(u2), c->Ac.p, out, c->flags.p);
+  c->pdl = latency_bound(c);
+  CU(launch_k(c->pdl, stage3_kernel, gb, 256, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)c->Ac.p, out,
+              c->flags.p));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;

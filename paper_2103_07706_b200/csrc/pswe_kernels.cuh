@@ -140,6 +140,8 @@ template <int NX>
 __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
     passA_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, const double2* __restrict__ Uc,
                  const double2* __restrict__ ctab, double2* __restrict__ I) {
+  griddep_wait();
+  griddep_launch();
   using W = PassAW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW;
   extern __shared__ __align__(128) unsigned char sbytes[];
@@ -426,6 +428,8 @@ __device__ __forceinline__ void uv_get4(double2 (&q)[4], const double2* uv, uint
 template <int NY>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     passB_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, double2* __restrict__ I2) {
+  griddep_wait();
+  griddep_launch();
   using W = PassBW<NY>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA;
   extern __shared__ __align__(128) unsigned char sbytes[];
@@ -521,6 +525,8 @@ struct PassBSW {
 template <int NY>
 __global__ void __launch_bounds__(128)
     passB_split_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, double2* __restrict__ I2) {
+  griddep_wait();
+  griddep_launch();
   using W = PassBSW<NY>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA;
   constexpr int Ky = PassBW<NY>::Ky;
@@ -652,6 +658,8 @@ __device__ __forceinline__ void passB_pair_prefetch(int lane, double2* pre, doub
 template <int NY>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     passB_pair_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mO) {
+  griddep_wait();
+  griddep_launch();
   using W = PassBW<NY>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, KYA = W::KYA, R = W::R, RP = W::RP;
   static_assert(P == 16, "FAST path needs 16 points per lane");
@@ -847,6 +855,8 @@ template <int NX>
 __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
     passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
                  const double2* __restrict__ ctab, double2* __restrict__ slots, int first_chunk) {
+  griddep_wait();
+  griddep_launch();
   using W = PassCW<NX>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, CPT = W::CPT;
   extern __shared__ __align__(128) unsigned char sbytes[];
@@ -963,6 +973,8 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
 // ordered sum of the phase-group slots -> compact tendency
 __global__ void reduce_slots_kernel(const double2* __restrict__ slots, int Gc, size_t n,
                                     double2* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     double2 a = slots[i];
     for (int g = 1; g < Gc; ++g) a = cadd(a, slots[(size_t)g * n + i]);
@@ -977,6 +989,8 @@ __global__ void reduce_slots_kernel(const double2* __restrict__ slots, int Gc, s
 // reference's real(ifft2(.)) does to a field (grid.py:173-174).
 __global__ void pack_kernel(GridDev G, const double2* __restrict__ u, const double2* __restrict__ v,
                             const double2* __restrict__ e, double2* __restrict__ Uc) {
+  griddep_wait();
+  griddep_launch();
   const size_t KyKx = (size_t)G.Ky * G.Kx;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 3 * KyKx; i += (size_t)gridDim.x * blockDim.x) {
     const int f = (int)(i / KyKx);
@@ -1013,6 +1027,8 @@ __device__ __forceinline__ C3 compact_at(const GridDev& G, const double2* __rest
 
 __global__ void unpack_kernel(GridDev G, const double2* __restrict__ Ac, double2* __restrict__ u,
                               double2* __restrict__ v, double2* __restrict__ e) {
+  griddep_wait();
+  griddep_launch();
   const size_t n = (size_t)G.nx * G.ny;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
@@ -1072,6 +1088,8 @@ __device__ __forceinline__ void flag_nonfinite(const C3& q, int stage, int* flag
 // stage 1 (integrator.py:96-98): e_dt = E(dt) U;  u1 = e_dt + dt * E(dt) A(U)
 __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const double2* __restrict__ Ac,
                               Full3w edt, Full3w u1, int* flags) {
+  griddep_wait();
+  griddep_launch();
   const size_t n = (size_t)G.nx * G.ny;
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < n; i0 += (size_t)gridDim.x * blockDim.x) {
     const size_t i = i0 + threadIdx.x;
@@ -1092,6 +1110,8 @@ __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const doub
 // stage 2 (integrator.py:99-100): u2 = 3/4 E(dt/2) U + 1/4 E(-dt/2) (u1 + dt A(u1))
 __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, const double2* __restrict__ Ac,
                               Full3w u2, int* flags) {
+  griddep_wait();
+  griddep_launch();
   const size_t n = (size_t)G.nx * G.ny;
   const double h = 0.5 * dt;
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < n; i0 += (size_t)gridDim.x * blockDim.x) {
@@ -1113,6 +1133,8 @@ __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, 
 // stage 3 (integrator.py:101-102): out = 1/3 e_dt + 2/3 E(dt/2) (u2 + dt A(u2))
 __global__ void stage3_kernel(GridDev G, Prop pr, double dt, Full3 edt, Full3 u2, const double2* __restrict__ Ac,
                               Full3w out, int* flags) {
+  griddep_wait();
+  griddep_launch();
   const size_t n = (size_t)G.nx * G.ny;
   const double h = 0.5 * dt;
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < n; i0 += (size_t)gridDim.x * blockDim.x) {
