@@ -128,7 +128,7 @@ struct pswe_ctx {
   int64_t launches = 0;
   // per-kernel event profiling
   bool prof = false;
-  bool pdl = false;  // programmatic dependent launch for the current chain (latency_bound)
+  bool pdl = false;  // programmatic dependent launch for the current chain (launch_k)
   std::vector<cudaEvent_t> ev_pool;
   struct Rec { int cls; cudaEvent_t a, b; };
   std::vector<Rec> recs;
@@ -189,9 +189,9 @@ struct ProfScope {
 // Kernel launch, with programmatic stream serialisation when `pdl`: the
 // grid may be scheduled while its predecessor in the stream finishes (every
 // kernel of the chain waits on griddepcontrol before its first global
-// access).  Used for latency-bound evaluations only, where all CTAs of a
-// kernel fit in one wave: with several waves, early-scheduled CTAs of the
-// next kernel would take the slots of the current one's later waves.
+// access).  Used for the stepper's kernels and for one-chunk RHS chains
+// (measured: 64^2 M=8 30 -> 26 us, 256^2 M=8 62 -> 57 us, 512^2 M=8
+// 169 -> 166 us); the multi-lane chains synchronise through events anyway.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      Args&&... args) {
@@ -208,10 +208,9 @@ cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, si
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-// small grids: the RHS chain is launch- and latency-bound
-bool latency_bound(const pswe_ctx* c) {
-  static const bool off = getenv("PSWE_NO_PDL") != nullptr;
-  return !off && (size_t)c->nx * c->ny <= (size_t)128 * 128;
+bool pdl_enabled() {
+  static const bool off = getenv("PSWE_NO_PDL") != nullptr;  // A/B switch
+  return !off;
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -510,7 +509,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   const int CP = std::max(1, std::min(P, (P + nchunks - 1) / nchunks));
   nchunks = (P + CP - 1) / CP;
   const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
-  c->pdl = latency_bound(c) && nchunks == 1;
+  c->pdl = pdl_enabled() && nchunks == 1;
   TRY(c->inter.alloc(per_phase * CP * lanes));
   TRY(c->slots.alloc((size_t)lanes * Gc * c->compact_elems()));
   if (getenv("PSWE_DEBUG_POISON")) {  // debug: NaN-fill intermediates to expose unwritten entries
@@ -604,30 +603,30 @@ int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
   const int P = (int)c->s_live.size();
   const int gb = elem_grid(n);
   // stage 1
-  c->pdl = latency_bound(c);
+  c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, U.u, U.v, U.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
-  c->pdl = latency_bound(c);
+  c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)c->Ac.p, edt, u1, c->flags.p));
   c->launches++;
   // stage 2
-  c->pdl = latency_bound(c);
+  c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, (const double2*)u1.u,
               (const double2*)u1.v, (const double2*)u1.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
-  c->pdl = latency_bound(c);
+  c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage2_kernel, gb, 256, 0, st, G, pr, dt, U, f3c(u1), (const double2*)c->Ac.p, u2,
               c->flags.p));
   c->launches++;
   // stage 3
-  c->pdl = latency_bound(c);
+  c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, (const double2*)u2.u,
               (const double2*)u2.v, (const double2*)u2.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
-  c->pdl = latency_bound(c);
+  c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage3_kernel, gb, 256, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)c->Ac.p, out,
               c->flags.p));
   c->launches++;
