@@ -344,3 +344,31 @@ def test_chebyshev_route_step_and_run_match_oracle():
     err = rel_l2(arr(got), want)
     print(f"chebyshev 3-step run rel L2 vs oracle {err:.3e}")
     assert err <= STEP_TOL
+
+
+def test_latency_paths_are_bitwise_identical(tmp_path):
+    """The latency-bound paths (split pass B, programmatic dependent launch)
+    change scheduling only: a run with both switched off (fresh process, the
+    switches are read once) gives the same bits for a C2 RHS and step."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2103_07706_b200 as pk\n"
+        "from paper_2103_07706_b200 import cases\n"
+        "c = cases.case_c2()\n"
+        "a = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())\n"
+        "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
+        "s = pk.step_averaged_ssprk3(c.state, cfg, c.params)\n"
+        "np.save(sys.argv[1], np.stack([a.u, a.v, a.eta, s.u, s.v, s.eta]))\n" % str(ROOT))
+    outs = []
+    for i, env in enumerate(({}, {"PSWE_NO_SPLIT": "1", "PSWE_NO_PDL": "1"})):
+        f = tmp_path / f"r{i}.npy"
+        p = subprocess.run([sys.executable, "-c", code, str(f)], env={**__import__("os").environ, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
