@@ -12,8 +12,13 @@ phases.  metric = P * 3 n^2 * steps / device seconds, summed over replicas.
 Multi-GPU: the path is run as independent replicas (north_star: no
 multi-GPU path); under torchrun every rank times its own replica, the time is
 the max over ranks and value = all ranks' units / that time ("scaling": "weak").
---impl reference times the oracle port of the reference (oracle/pswe_oracle.py,
-numpy + all host threads) on bounded phase samples of the same workload.
+`--gpus N` without a launcher re-executes itself under torch.distributed.run.
+--impl reference times the unmodified reference (phaseswe, installed into
+oracle/_ref by oracle/build_ref.sh) on the host cores on bounded phase samples
+of the same workload; the numpy port (oracle/pswe_oracle.py) stands in only
+when the reference is absent.  The default run's `cpu_baseline` evaluates the
+whole workload with the reference on all host cores and checks the GPU output
+against it (`parity`).
 """
 
 from __future__ import annotations
@@ -165,53 +170,168 @@ def oracle_sample(case, nodes, threads):
     return time.perf_counter() - t0, len(nodes)
 
 
-def cpu_baseline(case, budget_s: float = 12.0, threads: int | None = None) -> dict:
-    """Bounded CPU sample of the same workload: consecutive live nodes until ~budget_s."""
+def host_info(threads):
+    import platform
+    import scipy
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "threads_used": threads, "host_threads": os.cpu_count(),
+            "numpy": np.__version__, "scipy": scipy.__version__,
+            "blas_threads_env": {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                                               "MKL_NUM_THREADS")}}
+
+
+def _ref_eval(R, prob, quad, threads):
+    """The reference's public averaged_tendency (averaging.py:116-156) with a
+    ThreadPoolExecutor of `threads` workers (None = its serial path)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from phaseswe import averaging
+    if threads is None:
+        t0 = time.perf_counter()
+        out = averaging.averaged_tendency(prob.state, quad, prob.params, prob.spec)
+        return time.perf_counter() - t0, out
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        t0 = time.perf_counter()
+        out = averaging.averaged_tendency(prob.state, quad, prob.params, prob.spec, executor=ex)
+        return time.perf_counter() - t0, out
+
+
+def cpu_baseline(case, gpu_fields=None, one_core_budget_s: float = 6.0) -> dict:
+    """The reference on the host cores, same run (SURVEY.md 8d CPU plan).
+
+    * C cores: the reference's averaged_tendency over ALL live phases of the
+      benchmarked workload with a ThreadPoolExecutor(C) -- the unsampled
+      figure -- and its result is the parity check of the GPU output
+      (`parity`, rel L2 over (u, v, eta), tolerance 1e-10).
+    * 1 core: the reference's serial path (executor=None) on the 2m+1
+      central nodes, m sized for about `one_core_budget_s`.
+    Falls back to the numpy port (oracle/pswe_oracle.py) when the reference
+    is not installed (oracle/build_ref.sh)."""
+    from oracle import reference as R
+    threads = cpu_threads()
+    prob = R.problem(case)
+    info = host_info(threads)
+    if prob is None:
+        from oracle import pswe_oracle as O
+        g, p = case.grid, case.params
+        S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, p.f, p.g, p.H, p.b)
+        q = case.quadrature
+        t0 = time.perf_counter()
+        want = O.averaged_tendency(S, np.stack([case.state.u, case.state.v, case.state.eta]), q.s, q.w,
+                                   workers=threads)
+        used = time.perf_counter() - t0
+        out = {"value": case.P * case.dof / used, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"oracle/pswe_oracle.py averaged_tendency over all {case.P} live phases of {case.name}, "
+                         f"{threads} threads, {used:.1f} s (reference not installed)", "host": info}
+    else:
+        used, got = _ref_eval(R, prob, prob.quadrature, threads)
+        want = np.stack([got.u, got.v, got.eta])
+        out = {"value": case.P * case.dof / used, "unit": UNIT, "cores": threads, "kind": "reference",
+               "sample": f"phaseswe.averaging.averaged_tendency (unmodified reference, {R.where()}) over all "
+                         f"{case.P} live phases of {case.name} ({case.grid.nx}^2), ThreadPoolExecutor({threads}), "
+                         f"{used:.1f} s", "host": info}
+        # 1 core: the serial path on a central block of nodes
+        t1, _ = _ref_eval(R, prob, prob.sub_quadrature(1), None)
+        m = max(1, min(case.M - 1, int(one_core_budget_s / max(t1 / 3, 1e-6) / 2)))
+        q1 = prob.sub_quadrature(m)
+        t1, _ = _ref_eval(R, prob, q1, None)
+        ph = int(np.count_nonzero(q1.w))
+        out["one_core"] = {"value": ph * case.dof / t1, "unit": UNIT, "cores": 1,
+                           "sample": f"executor=None on the {ph} central nodes (renormalised sub-quadrature), "
+                                     f"{t1:.1f} s"}
+    if gpu_fields is not None:
+        diff = np.sqrt(sum(np.sum(np.abs(a - b) ** 2) for a, b in zip(gpu_fields, want)))
+        norm = np.sqrt(sum(np.sum(np.abs(b) ** 2) for b in want))
+        out["parity"] = {"rel_l2": float(diff / norm), "tol": 1e-10, "against": out["kind"],
+                         "what": "GPU averaged RHS of the timed workload vs the CPU evaluation above"}
+    return out
+
+
+def cpu_step_runs(threads=None, full_budget_s=60.0) -> list:
+    """C2-C4 on the host cores: the reference's step_averaged_ssprk3
+    (integrator.py:83-103) per step and its run(..., workers=C)
+    (integrator.py:145-183); a full run is timed when one step times the
+    step count fits `full_budget_s`, otherwise extrapolated (marked)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import reference as R
+    from paper_2103_07706_b200 import cases
+    if R.load() is None:
+        return []
+    from phaseswe import integrator
     threads = threads or cpu_threads()
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    live = [i for i in range(len(case.quadrature.w)) if case.quadrature.w[i] != 0.0]
-    batch = max(1, min(threads, len(live)))
-    used, phases, start = 0.0, 0, 0
-    while used < budget_s and start < len(live):
-        nodes = live[start:start + batch]
-        dt, k = oracle_sample(case, nodes, threads)
-        used += dt
-        phases += k
-        start += batch
-    value = phases * case.dof / used
-    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"oracle/pswe_oracle.py averaged_tendency on {phases} of {case.P} live phases of "
-                      f"{case.name} ({case.grid.nx}^2), {threads} threads, {used:.1f} s"}
+    out = []
+    for name in ("C2", "C3", "C4"):
+        c = cases.CASES[name]()
+        prob = R.problem(c)
+        cfg = integrator.StepConfig(dt=c.dt, quadrature=prob.quadrature, propagator_spec=prob.spec)
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            t0 = time.perf_counter()
+            integrator.step_averaged_ssprk3(prob.state, cfg, prob.params, ex)
+            step_s = time.perf_counter() - t0
+        ent = {"config": name, "grid": c.grid.nx, "M": c.M, "P": c.P, "steps": c.nsteps, "cores": threads,
+               "step_s": step_s, "phase_dof_per_s": 3 * c.P * c.dof / step_s}
+        if step_s * c.nsteps <= full_budget_s:
+            t0 = time.perf_counter()
+            integrator.run(prob.state, cfg, prob.params, t_end=c.nsteps * c.dt, workers=threads)
+            ent["run_s"] = time.perf_counter() - t0
+        else:
+            ent["run_s_extrapolated"] = step_s * c.nsteps
+        out.append(ent)
+    return out
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the oracle port of the reference on the host cores (rank 0 only)."""
+    """--impl reference: the unmodified reference (oracle/_ref phaseswe) on the
+    host cores, rank 0 only; every step is the reference's public
+    averaged_tendency on a bounded sample of the workload (the 2m+1 central
+    nodes, ~2 per core, weights renormalised), ThreadPoolExecutor(all
+    cores).  Falls back to the numpy port if the reference is absent."""
     if rank != 0:
         return
+    from oracle import reference as R
     from paper_2103_07706_b200 import cases
     case = cases.case_c5(args.level, args.M)
     threads = cpu_threads()
-    live = [i for i in range(len(case.quadrature.w)) if case.quadrature.w[i] != 0.0]
-    per_step = max(1, min(len(live), threads))
-    for _ in range(args.warmup):
-        oracle_sample(case, live[:per_step], threads)
-    total, phases = 0.0, 0
-    for k in range(args.steps):
-        start = (k * per_step) % len(live)
-        nodes = (live + live)[start:start + per_step]
-        dt, p = oracle_sample(case, nodes, threads)
-        total += dt
-        phases += p
-    value = phases * case.dof / total
+    prob = R.problem(case)
+    if prob is not None:
+        m = max(1, min(case.M - 1, threads))
+        quad = prob.sub_quadrature(m)
+        per_step = int(np.count_nonzero(quad.w))
+        for _ in range(args.warmup):
+            _ref_eval(R, prob, quad, threads)
+        total = 0.0
+        for _ in range(args.steps):
+            total += _ref_eval(R, prob, quad, threads)[0]
+        kind = "reference"
+        sample = (f"phaseswe.averaging.averaged_tendency (unmodified reference, {R.where()}) on the {per_step} "
+                  f"central of {case.P} live phases per step (renormalised sub-quadrature), "
+                  f"ThreadPoolExecutor({threads})")
+    else:
+        live = [i for i in range(len(case.quadrature.w)) if case.quadrature.w[i] != 0.0]
+        per_step = max(1, min(len(live), threads))
+        for _ in range(args.warmup):
+            oracle_sample(case, live[:per_step], threads)
+        total = 0.0
+        for k in range(args.steps):
+            start = (k * per_step) % len(live)
+            total += oracle_sample(case, (live + live)[start:start + per_step], threads)[0]
+        kind = "port"
+        sample = f"{per_step} of {case.P} live phases per step, oracle/pswe_oracle.py, {threads} threads"
+    value = per_step * args.steps * case.dof / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded planar C5 stand-in, SURVEY.md 8d)",
         "config": workload_config(case),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{per_step} of {case.P} live phases per step, oracle/pswe_oracle.py, "
-                                   f"{threads} threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+                         "host": host_info(threads)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -407,8 +527,14 @@ def run_ours(args, ws, rank, local):
         steps_info = run_step_configs(pk, cases, torch, stream)
 
     cpu = None
+    cpu_steps = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_baseline(case, budget_s=args.cpu_budget)
+        # the timed evaluation's output, checked against the CPU evaluation
+        ctx.averaged_tendency_compact(Uc, Ac)
+        gpu_fields = [t.cpu().numpy() for t in ctx.unpack(Ac)]
+        cpu = cpu_baseline(case, gpu_fields)
+        if not args.no_cpu_steps:
+            cpu_steps = cpu_step_runs()
 
     if rank == 0:
         line = {
@@ -421,6 +547,10 @@ def run_ours(args, ws, rank, local):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "gpu": torch.cuda.get_device_name(local), "sweep": sweep, "step_configs": steps_info,
         }
+        if cpu is not None and "parity" in cpu:
+            line["parity"] = cpu["parity"]
+        if cpu_steps:
+            line["cpu_step_configs"] = cpu_steps
         if sharded is not None:
             line["phase_sharded"] = sharded
         print(json.dumps(line), flush=True)
@@ -565,7 +695,7 @@ def main():
     ap.add_argument("--level", type=int, default=7)
     ap.add_argument("--M", type=int, default=256)
     ap.add_argument("--e2e-steps", type=int, default=30)
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-steps", action="store_true", help="skip the reference's C2-C4 CPU step timings")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
@@ -575,7 +705,18 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # no launcher: start one rank per GPU ourselves (same command under torchrun)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py")] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE = {ws}; launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return

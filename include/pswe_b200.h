@@ -129,6 +129,19 @@ double pswe_max_frequency(const pswe_ctx* ctx);
 /* Number of kernels this context has launched (instrumentation). */
 int64_t pswe_launch_count(const pswe_ctx* ctx);
 
+/* Launches per kernel variant (instrumentation: which code path ran), graph
+ * replays included.  Variants: */
+#define PSWE_V_PASSA 0        /* pass A (e^{sL} + inverse x-FFTs) */
+#define PSWE_V_PASSB_PAIR 1   /* pass B, phase-paired, TMEM stash + TMA tile stores */
+#define PSWE_V_PASSB_ROW 2    /* pass B, one phase per warp */
+#define PSWE_V_PASSB_SPLIT 3  /* pass B, a row group's transforms over four warps */
+#define PSWE_V_PASSC 4        /* pass C (forward x-FFTs, e^{-sL}, weighted sum) */
+#define PSWE_V_REDUCE 5       /* ordered slot reduction */
+#define PSWE_V_FUSED 6        /* fused one-CTA-per-phase small-grid kernel */
+#define PSWE_V_HERM 7         /* exact Hermitian-defect check (error path) */
+#define PSWE_NUM_VARIANTS 8
+int pswe_variant_launches(const pswe_ctx* ctx, int64_t* counts, int n);
+
 /* Snapshot diagnostics of a full-layout state (Trajectory.record,
  * integrator.py:124-135, and energy_mass, diagnostics.py:58-78): physical
  * fields by a full 2-D C2R on the device (Hermitian part, as real(ifft2)),

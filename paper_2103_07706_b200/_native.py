@@ -55,6 +55,7 @@ SIGNATURES = {
     "pswe_run": (_i, [_vp, _d, _i, _vp, _vp, _vp, _c_int_p, _c_int_p, _c_int_p, _vp]),
     "pswe_max_frequency": (_d, [_vp]),
     "pswe_launch_count": (ctypes.c_int64, [_vp]),
+    "pswe_variant_launches": (_i, [_vp, ctypes.POINTER(ctypes.c_int64), _i]),
     "pswe_diagnostics": (_i, [_vp, _vp, _vp, _vp, ctypes.POINTER(_d), _vp]),
     "pswe_to_physical": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_copy_band": (_i, [_vp, _i, _vp, _vp, _i, _vp]),
@@ -66,6 +67,7 @@ SIGNATURES = {
 }
 
 KERNEL_CLASSES = ("passA", "passB", "passC", "reduce", "pack", "unpack", "stage")
+VARIANTS = ("passA", "passB_pair", "passB_row", "passB_split", "passC", "reduce", "fused", "herm")
 
 
 class NativeError(RuntimeError):
@@ -122,6 +124,11 @@ def _dptr(t) -> ctypes.c_void_p:
 def _stream(torch):
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
+
+_libc = ctypes.CDLL(None)
+_memcmp = _libc.memcmp
+_memcmp.restype = ctypes.c_int
+_memcmp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
 
 _PIN = threading.local()  # per-thread pinned staging buffers for uploads
 
@@ -290,7 +297,6 @@ class Context:
         self.Ky, self.Kx = ky.value, kx.value
         self._quad_key = None
         self._prop_key = None
-        self._b_obj = None
         self._b_copy = None
 
     def __del__(self):
@@ -307,6 +313,13 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(_lib.pswe_launch_count(self.h))
+
+    @property
+    def variant_launches(self) -> dict:
+        """{kernel variant: launches so far} (which code paths ran)."""
+        cnt = (ctypes.c_int64 * len(VARIANTS))()
+        _check(_lib.pswe_variant_launches(self.h, cnt, len(VARIANTS)))
+        return {k: int(cnt[i]) for i, k in enumerate(VARIANTS)}
 
     def profile(self, enable: bool) -> None:
         _check(_lib.pswe_profile_enable(self.h, 1 if enable else 0))
@@ -355,17 +368,17 @@ class Context:
         self._prop_key = key
 
     def set_topography(self, b) -> None:
-        """Upload b (full spectral layout) unless this exact content is already set."""
-        if b is self._b_obj:
-            return
-        arr = np.asarray(b, dtype=np.complex128)
-        if self._b_copy is not None and self._b_copy.shape == arr.shape and np.array_equal(self._b_copy, arr):
-            self._b_obj = b
+        """Upload b (full spectral layout) unless this exact content is already
+        on the device.  The content is compared on every call (memcmp against
+        the copy taken at the last upload), so a b changed in place between
+        calls is picked up, as the reference reads params.b on every call."""
+        arr = np.ascontiguousarray(b, dtype=np.complex128)
+        if (self._b_copy is not None and self._b_copy.shape == arr.shape
+                and _memcmp(self._b_copy.ctypes.data, arr.ctypes.data, arr.nbytes) == 0):
             return
         bt = self.to_device(arr)
         _check(_lib.pswe_set_topography(self.h, _dptr(bt), _stream(self.torch)))
         self.torch.cuda.current_stream().synchronize()
-        self._b_obj = b
         self._b_copy = arr.copy()
 
     # ---- tensors ---------------------------------------------------------

@@ -82,6 +82,7 @@ struct DevBuf {
 
 struct pswe_ctx {
   int device = 0;
+  int sms = 148;  // multiprocessor count of the device (queried at create)
   int nx = 0, ny = 0, kxm = 0, kym = 0, Kx = 0, Ky = 0;
   double Lx = 0, Ly = 0, f = 0, g = 0, H = 0;
   double lam_max = 0;
@@ -126,6 +127,8 @@ struct pswe_ctx {
   DevBuf<int> flags;
   int* flags_host = nullptr;
   int64_t launches = 0;
+  int64_t variant[PSWE_NUM_VARIANTS] = {};        // launches per kernel variant
+  int64_t graph_variant[PSWE_NUM_VARIANTS] = {};  // ... inside one captured step graph
   // per-kernel event profiling
   bool prof = false;
   bool pdl = false;  // programmatic dependent launch for the current chain (launch_k)
@@ -152,9 +155,10 @@ struct pswe_ctx {
 
 namespace {
 
-int elem_grid(size_t n) {
+// elementwise grids: 256-thread blocks, at most 16 resident waves' worth
+int elem_grid(const pswe_ctx* c, size_t n) {
   size_t b = (n + 255) / 256;
-  return (int)std::max<size_t>(1, std::min<size_t>(b, 148 * 16));
+  return (int)std::max<size_t>(1, std::min<size_t>(b, (size_t)c->sms * 16));
 }
 
 // optional per-launch event bracketing: PROF_BEGIN before a launch, PROF_END after
@@ -221,12 +225,11 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
   auto kern = passA_kernel<NX>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int nblk = ((np + 1) / 2) * ((c->Ky + W::GPW - 1) / W::GPW);
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  const int blocks = std::min(nblk, W::CTAS * sms);
+  const int blocks = std::min(nblk, W::CTAS * c->sms);
   ProfScope ps(c, 0, st);
   CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, I1));
   c->launches++;
+  c->variant[PSWE_V_PASSA]++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
@@ -246,6 +249,7 @@ int launchB_small(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cuda
   ProfScope ps(c, 1, st);
   CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), np, mI1, I2));
   c->launches++;
+  c->variant[PSWE_V_PASSB_ROW]++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
@@ -260,6 +264,7 @@ int launchB_split(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cuda
   ProfScope ps(c, 1, st);
   CU(launch_k(c->pdl, kern, blocks, 128, smem, st, c->grid(), np, mI1, I2));
   c->launches++;
+  c->variant[PSWE_V_PASSB_SPLIT]++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
@@ -275,6 +280,7 @@ int launchB_pair(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap&
   ProfScope ps(c, 1, st);
   CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), np, mI1, mO));
   c->launches++;
+  c->variant[PSWE_V_PASSB_PAIR]++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
@@ -289,16 +295,14 @@ template <int NY>
 int launchB(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2,
             cudaStream_t st) {
   if constexpr (NY >= 64) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int sms = c->sms;
     const long long pair_ctas = (long long)lanes * ((np + 1) / 2) * c->nx / PassBW<NY>::GPC;
     if (passB_fast(c) && pair_ctas >= sms + sms / 3) return launchB_pair<NY>(c, np, mI1, mO, st);
   }
   // fewer single-phase CTAs than SMs: split each row group's transforms over
   // four warps (passB_split_kernel, two transform latencies instead of six)
   {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int sms = c->sms;
     const long long small_ctas = (long long)lanes * ((np * c->nx + PassBW<NY>::GPC - 1) / PassBW<NY>::GPC);
     if (small_ctas < sms && !getenv("PSWE_NO_SPLIT")) return launchB_split<NY>(c, np, mI1, I2, st);
   }
@@ -316,8 +320,7 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
                                                     PassCW<NX>::bytes(c->Kx)) != cudaSuccess ||
       per_sm < 1)
     per_sm = 3;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int sms = c->sms;
   const int slots = per_sm * sms;
   int best = 1;
   double best_eff = 0.0;
@@ -350,6 +353,7 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), c->prop(), ph, p0, np, Gc, I2, c->ctab_cur,
               slots, first));
   c->launches++;
+  c->variant[PSWE_V_PASSC]++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
@@ -482,7 +486,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     bool& valid = q ? c->ctab_q_valid : c->ctab_0_valid;
     if (!valid) {
       TRY(tb.alloc((size_t)P * c->Ky * c->Kx));
-      phase_table_kernel<<<elem_grid((size_t)P * c->Ky * c->Kx), 256, 0, st>>>(c->grid(), s, P, tb.p);
+      phase_table_kernel<<<elem_grid(c, (size_t)P * c->Ky * c->Kx), 256, 0, st>>>(c->grid(), s, P, tb.p);
       c->launches++;
       CU(cudaGetLastError());
       valid = true;
@@ -548,8 +552,9 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   if (direct) return PSWE_OK;
   const size_t n = c->compact_elems();
   ProfScope ps(c, 3, st);
-  CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(n), 256, 0, st, (const double2*)c->slots.p, lanes * Gc, n, Ac));
+  CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, n), 256, 0, st, (const double2*)c->slots.p, lanes * Gc, n, Ac));
   c->launches++;
+  c->variant[PSWE_V_REDUCE]++;
   CU(cudaGetLastError());
   return PSWE_OK;
 }
@@ -601,10 +606,10 @@ int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
   const GridDev G = c->grid();
   const Prop pr = c->prop();
   const int P = (int)c->s_live.size();
-  const int gb = elem_grid(n);
+  const int gb = elem_grid(c, n);
   // stage 1
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, U.u, U.v, U.e, c->Uc.p));
+  CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, U.u, U.v, U.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
   c->pdl = pdl_enabled();
@@ -612,7 +617,7 @@ int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
   c->launches++;
   // stage 2
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, (const double2*)u1.u,
+  CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, (const double2*)u1.u,
               (const double2*)u1.v, (const double2*)u1.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
@@ -622,7 +627,7 @@ int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
   c->launches++;
   // stage 3
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, elem_grid(c->compact_elems()), 256, 0, st, G, (const double2*)u2.u,
+  CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, (const double2*)u2.u,
               (const double2*)u2.v, (const double2*)u2.e, c->Uc.p));
   c->launches++;
   TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
@@ -657,6 +662,8 @@ int ensure_step_graph(pswe_ctx* c, double dt, Full3 Ain, Full3w Bout, size_t byt
   const bool prof = c->prof;
   c->prof = false;
   const int64_t l0 = c->launches;
+  int64_t v0[PSWE_NUM_VARIANTS];
+  std::copy(c->variant, c->variant + PSWE_NUM_VARIANTS, v0);
   CU(cudaStreamSynchronize(st));
   std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
   CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
@@ -676,6 +683,10 @@ int ensure_step_graph(pswe_ctx* c, double dt, Full3 Ain, Full3w Bout, size_t byt
   CU(ie);
   c->step_graph_launches = c->launches - l0;
   c->launches = l0;
+  for (int i = 0; i < PSWE_NUM_VARIANTS; ++i) {
+    c->graph_variant[i] = c->variant[i] - v0[i];
+    c->variant[i] = v0[i];
+  }
   c->graph_dt = dt;
   c->graph_version = c->version;
   c->graph_A = Ain.u;
@@ -707,6 +718,8 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
   CU(cudaSetDevice(device));
   pswe_ctx* c = new pswe_ctx();
   c->device = device;
+  if (cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || c->sms < 1)
+    c->sms = 148;
   c->nx = nx; c->ny = ny; c->Lx = Lx; c->Ly = Ly; c->f = f; c->g = g; c->H = H;
   c->kxm = nx / 3; c->kym = ny / 3;
   c->Kx = 2 * c->kxm + 1; c->Ky = c->kym + 1;
@@ -823,7 +836,7 @@ int pswe_set_topography(pswe_ctx* c, const double* b_dev, void* stream) {
   TRY(c->Uc.alloc(c->compact_elems()));
   const GridDev G = c->grid();
   const double2* b = (const double2*)b_dev;
-  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p);
+  pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p);
   c->launches++;
   CU(cudaMemcpyAsync(c->bc.p, c->Uc.p, (size_t)c->Ky * c->Kx * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   TRY(c->bfull.alloc(c->full_elems()));
@@ -902,7 +915,7 @@ int pswe_compact_shape(const pswe_ctx* c, int* Ky, int* Kx) {
 int pswe_pack(pswe_ctx* c, const double* u, const double* v, const double* e, double* Uc, void* stream) {
   if (!c || !u || !v || !e || !Uc) return set_err(PSWE_EINVAL, "null argument");
   CU(cudaSetDevice(c->device));
-  pack_kernel<<<elem_grid(c->compact_elems()), 256, 0, (cudaStream_t)stream>>>(
+  pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, (cudaStream_t)stream>>>(
       c->grid(), (const double2*)u, (const double2*)v, (const double2*)e, (double2*)Uc);
   c->launches++;
   CU(cudaGetLastError());
@@ -912,7 +925,7 @@ int pswe_pack(pswe_ctx* c, const double* u, const double* v, const double* e, do
 int pswe_unpack(pswe_ctx* c, const double* Uc, double* u, double* v, double* e, void* stream) {
   if (!c || !u || !v || !e || !Uc) return set_err(PSWE_EINVAL, "null argument");
   CU(cudaSetDevice(c->device));
-  unpack_kernel<<<elem_grid(c->full_elems()), 256, 0, (cudaStream_t)stream>>>(
+  unpack_kernel<<<elem_grid(c, c->full_elems()), 256, 0, (cudaStream_t)stream>>>(
       c->grid(), (const double2*)Uc, (double2*)u, (double2*)v, (double2*)e);
   c->launches++;
   CU(cudaGetLastError());
@@ -954,7 +967,7 @@ int pswe_apply_linear(pswe_ctx* c, const double* u, const double* v, const doubl
                       double* le, void* stream) {
   if (!c || !u || !v || !e || !lu || !lv || !le) return set_err(PSWE_EINVAL, "null argument");
   CU(cudaSetDevice(c->device));
-  linear_full_kernel<<<elem_grid(c->full_elems()), 256, 0, (cudaStream_t)stream>>>(c->grid(), f3(u, v, e),
+  linear_full_kernel<<<elem_grid(c, c->full_elems()), 256, 0, (cudaStream_t)stream>>>(c->grid(), f3(u, v, e),
                                                                                   f3w(lu, lv, le));
   c->launches++;
   CU(cudaGetLastError());
@@ -967,7 +980,7 @@ int pswe_propagate(pswe_ctx* c, double t, const double* u, const double* v, cons
   std::string msg;
   if (check_cheb(c, t, &msg) != PSWE_OK) return set_err(PSWE_EINVAL, "%s", msg.c_str());
   CU(cudaSetDevice(c->device));
-  propagate_full_kernel<<<elem_grid(c->full_elems()), 256, 0, (cudaStream_t)stream>>>(c->grid(), c->prop(), t,
+  propagate_full_kernel<<<elem_grid(c, c->full_elems()), 256, 0, (cudaStream_t)stream>>>(c->grid(), c->prop(), t,
                                                                                      f3(u, v, e), f3w(ou, ov, oe));
   c->launches++;
   CU(cudaGetLastError());
@@ -1066,6 +1079,7 @@ int pswe_run(pswe_ctx* c, double dt, int nsteps, double* u, double* v, double* e
       CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
       for (int j = 0; j < k; ++j) CU(cudaGraphLaunch(c->step_exec, st));
       c->launches += (int64_t)k * c->step_graph_launches;
+      for (int v = 0; v < PSWE_NUM_VARIANTS; ++v) c->variant[v] += (int64_t)k * c->graph_variant[v];
       CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
       if (*c->flags_host) {
@@ -1092,6 +1106,12 @@ done:
 double pswe_max_frequency(const pswe_ctx* c) { return c ? c->lam_max : 0.0; }
 
 int64_t pswe_launch_count(const pswe_ctx* c) { return c ? c->launches : 0; }
+
+int pswe_variant_launches(const pswe_ctx* c, int64_t* counts, int n) {
+  if (!c || !counts) return set_err(PSWE_EINVAL, "null argument");
+  for (int i = 0; i < n && i < PSWE_NUM_VARIANTS; ++i) counts[i] = c->variant[i];
+  return PSWE_OK;
+}
 
 // full 2-D C2R of (u, v, eta, b) with row partials of the diagnostics; phys
 // (optional) receives the physical u, v, eta

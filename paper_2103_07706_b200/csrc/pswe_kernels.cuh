@@ -502,8 +502,10 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   }
 }
 
-// Latency-bound small grids (NY <= 64, few rows in flight): the four
-// inverse transforms of a row group run on four warps at once instead of in
+// Latency-bound evaluations -- launchB picks this whenever the single-phase
+// CTAs of all lanes would not fill the SMs: small grids with few phases, but
+// also 256^2 / 512^2 with one phase (apply_nonlinear, step_reference).  The
+// four inverse transforms of a row group run on four warps at once instead of in
 // sequence -- warp w: 0 (u, v), 1 (ux, i ky u), 2 (vx, i ky v), 3 (depth) --
 // the physical values meet in shared memory, and warps 0 and 1 run the two
 // forward transforms (A + iB, C + iD) side by side: two transform latencies

@@ -121,9 +121,14 @@ def sharded_averaged_tendency(state, quadrature, params, propagator_spec, group=
     err, finish, part = None, None, None
     try:
         finish, part = (partial or device_partial)(state, quadrature, w_rank, params, propagator_spec)
-    except (ValueError, RuntimeError) as exc:
+    except Exception as exc:  # noqa: BLE001 -- every rank must reach the agreement collective below
         exc = node_error(exc)
-        err = ("value:" if isinstance(exc, ValueError) else "runtime:") + str(exc)
+        if isinstance(exc, ValueError):
+            err = "value:" + str(exc)
+        elif isinstance(exc, RuntimeError):
+            err = "runtime:" + str(exc)
+        else:
+            err = f"runtime:{type(exc).__name__}: {exc}"
     device = part.device if part is not None else (
         torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu"))
     first = _first_error(err, group, world, device)

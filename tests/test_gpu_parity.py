@@ -139,6 +139,47 @@ def test_c5_512_rhs_matches_oracle():
     assert err <= RHS_TOL
 
 
+def _oracle_rhs(c, U=None, workers=16):
+    g, q = c.grid, c.quadrature
+    S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, c.params.f, c.params.g, c.params.H, c.params.b)
+    return O.averaged_tendency(S, arr(c.state) if U is None else U, q.s, q.w, workers=workers)
+
+
+@pytest.mark.parametrize("level,M", [(7, 256), (6, 256)])
+def test_c5_benchmarked_rhs_matches_oracle(level, M):
+    """The benchmarked configuration itself: all 2M - 1 live phases (511 at
+    M = 256) through 4 lanes x several chunks, the phase-paired pass B and
+    the multi-slot reduction, against the oracle's full node sum
+    (averaging.py:128-156)."""
+    c = cases.case_c5(level, M)
+    got = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())
+    err = O.rel_l2(arr(got), _oracle_rhs(c))
+    print(f"C5 {c.grid.nx}^2 M={M} rel L2 vs oracle {err:.3e}")
+    assert err <= RHS_TOL
+
+
+@pytest.mark.parametrize("level", [4, 5, 6, 7])
+def test_c5_m128_unbalanced_matches_oracle(level):
+    """C5 states are balanced (e^{sL} U = U), which would hide a wrong phase
+    shift in pass A; here an unbalanced, band-limited perturbation of O(1)
+    relative size is added, so every phase's forward and backward
+    exponential matters.  M = 128 (255 phases): several chunks per lane,
+    every lane, phase pairs, several pass-C slots."""
+    c = cases.case_c5(level, 128)
+    g = c.grid
+    rng = np.random.default_rng(100 + level)
+    S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, c.params.f, c.params.g, c.params.H)
+    U = arr(c.state)
+    pert = np.stack([O.truncate(O.spectral(rng.standard_normal((g.nx, g.ny))), S.mask) for _ in range(3)])
+    for f in range(3):
+        pert[f] *= 0.5 * np.max(np.abs(U[f])) / np.max(np.abs(pert[f]))
+    U = U + pert
+    got = pk.averaged_tendency(state_from(U, g), c.quadrature, c.params, pk.PropagatorSpec.exact())
+    err = O.rel_l2(arr(got), _oracle_rhs(c, U))
+    print(f"C5 {g.nx}^2 M=128 unbalanced rel L2 vs oracle {err:.3e}")
+    assert err <= RHS_TOL
+
+
 def test_linearity_in_weights_at_512_m256():
     """Full-size property: A(w_even + w_odd) = A(w_even) + A(w_odd) over all 511 phases."""
     c = cases.case_c5(7, 256)
@@ -349,26 +390,60 @@ def test_chebyshev_route_step_and_run_match_oracle():
 def test_latency_paths_are_bitwise_identical(tmp_path):
     """The latency-bound paths (split pass B, programmatic dependent launch)
     change scheduling only: a run with both switched off (fresh process, the
-    switches are read once) gives the same bits for a C2 RHS and step."""
+    switches are read once) gives the same bits for a C2 RHS and step, and
+    for a single-node 512^2 nonlinearity (split pass B at NY = 512).  The
+    baseline run must really have taken the split path (variant counts)."""
+    import os
     import subprocess
     import sys
 
     from conftest import ROOT
 
     code = (
-        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import sys, json, numpy as np; sys.path.insert(0, %r)\n"
         "import paper_2103_07706_b200 as pk\n"
         "from paper_2103_07706_b200 import cases\n"
         "c = cases.case_c2()\n"
         "a = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())\n"
         "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
         "s = pk.step_averaged_ssprk3(c.state, cfg, c.params)\n"
-        "np.save(sys.argv[1], np.stack([a.u, a.v, a.eta, s.u, s.v, s.eta]))\n" % str(ROOT))
-    outs = []
+        "v = pk.dynamics.context(c.state, c.params).variant_launches\n"
+        "d = cases.case_c5(7, 8)\n"
+        "n = pk.apply_nonlinear(d.state, d.params)\n"
+        "v2 = pk.dynamics.context(d.state, d.params).variant_launches\n"
+        "np.save(sys.argv[1], np.stack([a.u, a.v, a.eta, s.u, s.v, s.eta]))\n"
+        "np.save(sys.argv[1] + '.512.npy', np.stack([n.u, n.v, n.eta]))\n"
+        "print(json.dumps([v, v2]))\n" % str(ROOT))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
+    outs, variants = [], []
     for i, env in enumerate(({}, {"PSWE_NO_SPLIT": "1", "PSWE_NO_PDL": "1"})):
         f = tmp_path / f"r{i}.npy"
-        p = subprocess.run([sys.executable, "-c", code, str(f)], env={**__import__("os").environ, **env},
+        p = subprocess.run([sys.executable, "-c", code, str(f)], env={**base, **env},
                            capture_output=True, text=True, timeout=300)
         assert p.returncode == 0, p.stderr
-        outs.append(np.load(f))
-    assert np.array_equal(outs[0], outs[1])
+        import json
+        variants.append(json.loads(p.stdout.strip().splitlines()[-1]))
+        outs.append((np.load(f), np.load(str(f) + ".512.npy")))
+    assert variants[0][0]["passB_split"] > 0 and variants[1][0]["passB_split"] == 0
+    assert variants[0][1]["passB_split"] > 0 and variants[1][1]["passB_split"] == 0
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("level", [6, 7])
+def test_single_node_large_grid_matches_oracle(level):
+    """One node on 256^2 / 512^2 (apply_nonlinear and the fine-step
+    reference's step): the split pass B at NY = 256 / 512 against the oracle."""
+    c = cases.case_c5(level, 8)
+    g = c.grid
+    rng = np.random.default_rng(level)
+    S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, c.params.f, c.params.g, c.params.H)
+    U = arr(c.state) + np.stack([O.truncate(O.spectral(sc * rng.standard_normal((g.nx, g.ny))), S.mask)
+                                 for sc in (1.0, 1.0, 50.0)])
+    st = state_from(U, g)
+    got = pk.apply_nonlinear(st, c.params)
+    assert O.rel_l2(arr(got), O.nonlinear(S, U)) <= 1e-12
+    one = pk.step_reference(st, 180.0, c.params)
+    assert O.rel_l2(arr(one), O.ssprk3_step(S, U, 180.0, [0.0], [1.0])) <= STEP_TOL
+    v = pk.dynamics.context(st, c.params).variant_launches
+    assert v["passB_split"] > 0

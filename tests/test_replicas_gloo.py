@@ -49,5 +49,28 @@ def test_reference_arm_runs_on_cpu_and_prints_contract_line():
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "cpu_baseline", "e2e", "config"):
         assert key in line
-    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"
+    from oracle import reference as R
+    want_kind = "reference" if R.load() is not None else "port"
+    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == want_kind
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0
+
+
+def test_cpu_baseline_leg_checks_parity():
+    """bench.py's cpu_baseline leg: the whole workload on the host cores
+    (the reference itself when oracle/_ref is built) and the rel-L2 parity
+    of a given result against it -- here the oracle port's own result."""
+    import numpy as np
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from oracle import pswe_oracle as O
+    from paper_2103_07706_b200 import cases
+    c = cases.case_c5(3, 4)  # 32^2, 7 phases
+    g, q = c.grid, c.quadrature
+    S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, c.params.f, c.params.g, c.params.H)
+    got = O.averaged_tendency(S, np.stack([c.state.u, c.state.v, c.state.eta]), q.s, q.w)
+    out = bench.cpu_baseline(c, list(got), one_core_budget_s=0.2)
+    assert out["value"] > 0 and out["cores"] >= 1
+    assert out["parity"]["rel_l2"] <= 1e-13 and out["parity"]["tol"] == 1e-10
+    assert "numpy" in out["host"] and "cpu_model" in out["host"]
+    if out["kind"] == "reference":
+        assert out["one_core"]["cores"] == 1

@@ -56,6 +56,14 @@ def _failing_partial(state, quadrature, w_rank, params, spec):
     return _oracle_partial(state, quadrature, w_rank, params, spec)
 
 
+def _odd_partial(state, quadrature, w_rank, params, spec):
+    from paper_2103_07706_b200.sharding import live_nodes
+
+    if int(live_nodes(w_rank)[0]) - quadrature.M > -quadrature.M + 3:  # rank 1 only
+        raise KeyError("boom")  # neither ValueError nor RuntimeError
+    return _oracle_partial(state, quadrature, w_rank, params, spec)
+
+
 def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     sys.path.insert(0, str(ROOT))
@@ -70,7 +78,13 @@ def _worker(rank, world, port, out):
         msg = None
     except RuntimeError as exc:
         msg = str(exc)
-    out.put((rank, np.stack([got.u, got.v, got.eta]), got.t, msg))
+    # any exception type on one rank is agreed on too (no rank left waiting)
+    try:
+        sharded_averaged_tendency(c.state, c.quadrature, c.params, None, partial=_odd_partial)
+        odd = None
+    except RuntimeError as exc:
+        odd = str(exc)
+    out.put((rank, np.stack([got.u, got.v, got.eta]), got.t, msg, odd))
     dist.destroy_process_group()
 
 
@@ -97,7 +111,8 @@ def test_sharded_sum_two_ranks_gloo():
     U = np.stack([c.state.u, c.state.v, c.state.eta])
     parts = [O.averaged_tendency(S, U, c.quadrature.s, shard_weights(c.quadrature.w, 2, r)) for r in range(2)]
     # every rank holds the same result: the partial sums added in rank order, bitwise
-    for rank, got, t, msg in res:
+    for rank, got, t, msg, odd in res:
+        assert odd == "KeyError: 'boom'"
         assert np.array_equal(got, parts[0] + parts[1])
         assert t == c.state.t
         # the failure of the first failing node (rank 1's first node) reaches both ranks
