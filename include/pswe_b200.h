@@ -43,6 +43,7 @@ extern "C" {
 #define PSWE_EUNSUPPORTED 3  /* grid size not supported by the GPU path */
 #define PSWE_ENONFINITE 4    /* non-finite state after a stage (integrator.py:77-80) */
 #define PSWE_ESTATE 5        /* call order violated (e.g. no quadrature set) */
+#define PSWE_EHERM 6         /* non-Hermitian spectral input (to_physical's gate, grid.py:159-172) */
 
 typedef struct pswe_ctx pswe_ctx;
 

@@ -25,6 +25,7 @@ PSWE_ECUDA = 2
 PSWE_EUNSUPPORTED = 3
 PSWE_ENONFINITE = 4
 PSWE_ESTATE = 5
+PSWE_EHERM = 6
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -102,7 +103,7 @@ def load_library(path: os.PathLike | None = None):
 def _check(rc: int) -> None:
     if rc != PSWE_OK:
         msg = _lib.pswe_last_error().decode("utf-8", "replace")
-        if rc in (PSWE_EINVAL, PSWE_EUNSUPPORTED):
+        if rc in (PSWE_EINVAL, PSWE_EUNSUPPORTED, PSWE_EHERM):
             err = ValueError(msg)
             err.code = rc
             raise err
@@ -205,18 +206,48 @@ def _zero_out_of_band(h, nx, ny):
     h[nx - kxm:, kym + 1:ny - kym].zero_()
 
 
-def download_fields(tensors, band_ctx=None):
+_FILL = None
+_FILL_LOCK = threading.Lock()
+
+
+def _filler():
+    global _FILL
+    with _FILL_LOCK:
+        if _FILL is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _FILL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="pswe-fill")
+        return _FILL
+
+
+def band_hosts_async(shape, count: int):
+    """Pinned host buffers for a band download, their out-of-band part
+    zero-filled on a helper thread -- meant to run while a synchronous C-ABI
+    call (which releases the GIL) waits for the device."""
+    def make():
+        hs = [_POOL_OUT.take(shape, _torch().complex128) for _ in range(count)]
+        for h in hs:
+            _zero_out_of_band(h, shape[0], shape[1])
+        return hs
+    return _filler().submit(make)
+
+
+def download_fields(tensors, band_ctx=None, hosts=None):
     """CUDA tensors -> numpy arrays backed by pooled pinned host memory (one
     stream sync, no host copy).  With ``band_ctx`` (a Context) the tensors are
     known to vanish outside the 2/3 band: only the band crosses the bus and
-    the host zero-fills the rest (before the copy is queued, while the device
-    is still busy)."""
+    the host zero-fills the rest (``hosts``: a band_hosts_async future whose
+    buffers are already zero-filled)."""
     torch = _torch()
-    hosts = [_POOL_OUT.take(t.shape, t.dtype) for t in tensors]
-    if band_ctx is not None and tensors:
+    if hosts is not None:
+        hosts = hosts.result()
+    elif band_ctx is not None:
+        hosts = [_POOL_OUT.take(t.shape, t.dtype) for t in tensors]
         nx, ny = tensors[0].shape
         for h in hosts:
             _zero_out_of_band(h, nx, ny)
+    else:
+        hosts = [_POOL_OUT.take(t.shape, t.dtype) for t in tensors]
+    if band_ctx is not None and tensors:
         _check(_lib.pswe_copy_band(band_ctx.h, 1, _ptrs([h.data_ptr() for h in hosts]),
                                    _ptrs([t.data_ptr() for t in tensors]), len(tensors), _stream(torch)))
     else:
@@ -298,6 +329,7 @@ class Context:
         self._quad_key = None
         self._prop_key = None
         self._b_copy = None
+        self._b_obj = None
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -372,14 +404,18 @@ class Context:
         on the device.  The content is compared on every call (memcmp against
         the copy taken at the last upload), so a b changed in place between
         calls is picked up, as the reference reads params.b on every call."""
+        if b is self._b_obj and isinstance(b, np.ndarray) and not b.flags.writeable and b.base is None:
+            return  # the same read-only array that owns its data: cannot have changed
         arr = np.ascontiguousarray(b, dtype=np.complex128)
         if (self._b_copy is not None and self._b_copy.shape == arr.shape
                 and _memcmp(self._b_copy.ctypes.data, arr.ctypes.data, arr.nbytes) == 0):
+            self._b_obj = b
             return
         bt = self.to_device(arr)
         _check(_lib.pswe_set_topography(self.h, _dptr(bt), _stream(self.torch)))
         self.torch.cuda.current_stream().synchronize()
         self._b_copy = arr.copy()
+        self._b_obj = b
 
     # ---- tensors ---------------------------------------------------------
     def to_device(self, arr):
@@ -457,13 +493,19 @@ class Context:
         return out
 
     def run(self, dt: float, nsteps: int, U):
-        """In-place nsteps on U (list of 3 tensors). Returns (bad_step, stage, field)."""
+        """In-place nsteps on U (list of 3 tensors). Returns (bad_step, stage, field)
+        for a non-finite stage; a step whose input fails the Hermitian gate
+        raises ValueError with ``bad_step`` set (1-based)."""
         bs, st, fl = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(-1)
         rc = _lib.pswe_run(self.h, float(dt), int(nsteps), *(_dptr(x) for x in U),
                            ctypes.byref(bs), ctypes.byref(st), ctypes.byref(fl), _stream(self.torch))
         if rc == PSWE_ENONFINITE:
             return bs.value, st.value, fl.value
-        _check(rc)
+        try:
+            _check(rc)
+        except ValueError as exc:
+            exc.bad_step = bs.value
+            raise
         return 0, 0, -1
 
 

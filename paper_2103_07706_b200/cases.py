@@ -97,8 +97,15 @@ def _cone(grid, b0, r0, xc, yc):
     return _spec(grid, b0 * (1.0 - np.minimum(r, r0) / r0))
 
 
+def _frozen(b):
+    # read-only topography: the drop-in then skips re-checking it per call
+    b = np.array(b, dtype=np.complex128)
+    b.setflags(write=False)
+    return b
+
+
 def _flat(grid):
-    return np.zeros((grid.nx, grid.ny), dtype=np.complex128)
+    return _frozen(np.zeros((grid.nx, grid.ny), dtype=np.complex128))
 
 
 def case_c1() -> Case:
@@ -150,7 +157,7 @@ def case_c3() -> Case:
     ceta = _balanced_eta(grid, cu, F0, G_EARTH)
     b = _cone(grid, 2000.0, A_EARTH * math.pi / 9.0, A_EARTH * math.pi / 2.0,
               y_of_lat(math.pi / 6.0))
-    params = PhysicsParams(f=F0, g=G_EARTH, H=H, b=b)
+    params = PhysicsParams(f=F0, g=G_EARTH, H=H, b=_frozen(b))
     st = State(grid=grid, u=cu, v=np.zeros_like(cu), eta=ceta, t=0.0)
     return Case("C3", grid, params, st, T_half=1800.0, M=32, dt=1800.0, nsteps=48)
 

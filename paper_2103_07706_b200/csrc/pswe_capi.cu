@@ -17,6 +17,7 @@
 #include "../../include/pswe_b200.h"
 #include "pswe_kernels.cuh"
 #include "diag_kernels.cuh"
+#include "herm_kernels.cuh"
 
 using namespace pswe;
 
@@ -126,6 +127,11 @@ struct pswe_ctx {
   DevBuf<double2> full_tmp;  // stepper: edt, u1, u2 (3 states) + run ping-pong (2 states)
   DevBuf<int> flags;
   int* flags_host = nullptr;
+  // Hermitian gate (herm_kernels.cuh): [0..2] pack statistics, [4..4+P) per-phase
+  // scales (kept zeroed between evaluations by herm_eval_kernel); exact-path output
+  DevBuf<double> hgate, hout;
+  size_t hgate_n = 0;
+  double bdef = 0.0;  // max |b(k) - conj b(-k)| over the band
   int64_t launches = 0;
   int64_t variant[PSWE_NUM_VARIANTS] = {};        // launches per kernel variant
   int64_t graph_variant[PSWE_NUM_VARIANTS] = {};  // ... inside one captured step graph
@@ -219,7 +225,8 @@ bool pdl_enabled() {
 
 // ---------------------------------------------------------------- dispatch
 template <int NX>
-int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, cudaStream_t st) {
+int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, double* pscale,
+            cudaStream_t st) {
   using W = PassAW<NX>;
   const size_t smem = W::bytes(c->Kx);
   auto kern = passA_kernel<NX>;
@@ -227,7 +234,8 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
   const int nblk = ((np + 1) / 2) * ((c->Ky + W::GPW - 1) / W::GPW);
   const int blocks = std::min(nblk, W::CTAS * c->sms);
   ProfScope ps(c, 0, st);
-  CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, I1));
+  CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), c->prop(), ph, p0, np, Uc, c->ctab_cur, I1,
+              pscale));
   c->launches++;
   c->variant[PSWE_V_PASSA]++;
   CU(cudaGetLastError());
@@ -358,15 +366,16 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   return PSWE_OK;
 }
 
-int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, cudaStream_t st) {
+int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, double* pscale,
+              cudaStream_t st) {
   switch (c->nx) {
-    case 8: return launchA<8>(c, ph, p0, np, Uc, I1, st);
-    case 16: return launchA<16>(c, ph, p0, np, Uc, I1, st);
-    case 32: return launchA<32>(c, ph, p0, np, Uc, I1, st);
-    case 64: return launchA<64>(c, ph, p0, np, Uc, I1, st);
-    case 128: return launchA<128>(c, ph, p0, np, Uc, I1, st);
-    case 256: return launchA<256>(c, ph, p0, np, Uc, I1, st);
-    case 512: return launchA<512>(c, ph, p0, np, Uc, I1, st);
+    case 8: return launchA<8>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 16: return launchA<16>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 32: return launchA<32>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 64: return launchA<64>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 128: return launchA<128>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 256: return launchA<256>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 512: return launchA<512>(c, ph, p0, np, Uc, I1, pscale, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
 }
@@ -476,8 +485,22 @@ int map_tiles_I2(const pswe_ctx* c, double2* I2, int CP, CUtensorMap* m) {
 
 // Averaged RHS on compact data: chunks of phases through passes A, B, C,
 // then the ordered slot reduction.  `P` live phases in (s, w) device arrays.
+// Hermitian gate scratch: zeroed once, kept zeroed by herm_eval_kernel
+int ensure_hgate(pswe_ctx* c, int P) {
+  const size_t need = 4 + (size_t)std::max(P, 1);
+  if (c->hgate_n >= need) return PSWE_OK;
+  TRY(c->hgate.alloc(need));
+  CU(cudaMemset(c->hgate.p, 0, need * sizeof(double)));
+  c->hgate_n = need;
+  return PSWE_OK;
+}
+
+// `gate_bit` >= 0: the input was packed with the gate's statistics
+// (pack_kernel hstat = hgate); pass A adds the per-phase scales and the
+// evaluation ends with herm_eval_kernel, which sets flags bit gate_bit when
+// the exact check has to decide.
 int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const double2* Uc, double2* Ac,
-                cudaStream_t st) {
+                cudaStream_t st, int gate_bit = -1) {
   // exact route: phase table (built once per quadrature / grid)
   c->ctab_cur = nullptr;
   if (c->kind == 0) {
@@ -541,7 +564,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     // a single slot (one chunk, Gc = 1, e.g. the fine-step reference's one
     // node) is the output itself: pass C writes it, no reduction launch
     double2* sl = direct ? Ac : c->slots.p + (size_t)L * Gc * c->compact_elems();
-    TRY(dispatchA(c, ph, p0, np, Uc, I1, lst[L]));
+    TRY(dispatchA(c, ph, p0, np, Uc, I1, gate_bit >= 0 ? c->hgate.p + 4 : nullptr, lst[L]));
     TRY(dispatchB(c, np, lanes, mrow[L], mcol[L], I2, lst[L]));
     TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
   }
@@ -549,13 +572,97 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     CU(cudaEventRecord(c->ev_lane[L - 1], lst[L]));
     CU(cudaStreamWaitEvent(st, c->ev_lane[L - 1], 0));
   }
-  if (direct) return PSWE_OK;
-  const size_t n = c->compact_elems();
-  ProfScope ps(c, 3, st);
-  CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, n), 256, 0, st, (const double2*)c->slots.p, lanes * Gc, n, Ac));
+  if (!direct) {
+    const size_t n = c->compact_elems();
+    ProfScope ps(c, 3, st);
+    CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, n), 256, 0, st, (const double2*)c->slots.p, lanes * Gc, n,
+                Ac));
+    c->launches++;
+    c->variant[PSWE_V_REDUCE]++;
+    CU(cudaGetLastError());
+  }
+  if (gate_bit >= 0) {
+    CU(launch_k(c->pdl, herm_eval_kernel, 1, 256, 0, st, c->hgate.p, c->bdef, c->hgate.p + 4, P, c->H, c->g,
+                c->flags.p, gate_bit));
+    c->launches++;
+    CU(cudaGetLastError());
+  }
+  return PSWE_OK;
+}
+
+// ---------------------------------------------------------------- Hermitian gate, exact path
+int herm_message(pswe_ctx* c, double worst, double ref, long long idx, std::string* msg) {
+  const int i = (int)(idx / c->ny), j = (int)(idx % c->ny);
+  const int wx = i < c->nx / 2 ? i : i - c->nx, wy = j < c->ny / 2 ? j : j - c->ny;
+  char buf[256];
+  snprintf(buf, sizeof(buf),
+           "non-Hermitian spectral field: mode (kx index %d, ky index %d) has asymmetry %.3e (relative %.3e)", wx,
+           wy, worst, worst / ref);
+  *msg = buf;
+  return PSWE_EHERM;
+}
+
+// The reference's gate at every node of (s_dev, s_host, k) in ascending order
+// on the full-layout state U (dynamics.py:159-164 inside averaging.py:130-141):
+// PSWE_EHERM with the first failing node's message (wrapped as the node
+// error when `k` is given), PSWE_OK when every node passes.  Nodes whose
+// propagated fields are not finite are left to the non-finite stage check.
+int exact_gate(pswe_ctx* c, const double* s_dev, const std::vector<double>& s_host, const std::vector<int>* k,
+               Full3 U, cudaStream_t st) {
+  const int P = (int)s_host.size();
+  TRY(c->hout.alloc((size_t)8 * P));
+  herm_node_kernel<256><<<P, 256, 0, st>>>(c->grid(), c->prop(), s_dev, U.u, U.v, U.e,
+                                           c->bfull.p ? (const double2*)c->bfull.p : nullptr, c->hout.p);
   c->launches++;
-  c->variant[PSWE_V_REDUCE]++;
+  c->variant[PSWE_V_HERM]++;
   CU(cudaGetLastError());
+  std::vector<double> h((size_t)8 * P);
+  CU(cudaMemcpyAsync(h.data(), c->hout.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (int p = 0; p < P; ++p) {
+    const double* o = h.data() + (size_t)8 * p;
+    const double ref = o[0];
+    if (o[7] != 0.0 || !(ref > 0.0)) continue;
+    for (int f = 0; f < 3; ++f) {
+      const double worst = o[1 + 2 * f];
+      if (worst > 1e-12 * ref) {
+        std::string m;
+        herm_message(c, worst, ref, (long long)o[2 + 2 * f], &m);
+        if (k)
+          return set_err(PSWE_EHERM, "averaging node k = %d (s = %.6g s) failed: %s", (*k)[p], s_host[p], m.c_str());
+        return set_err(PSWE_EHERM, "%s", m.c_str());
+      }
+    }
+  }
+  return PSWE_OK;
+}
+
+// The full-grid gate of to_physical as the snapshot paths call it
+// (diagnostics.py:21-25 + :72, integrator.py:126-129, io.py:41-46): u and v
+// against vel_scale = max(max|u|, max|v|), eta against itself, b (when
+// `with_b`) against itself, in that order.  Synchronises.
+int full_gate(pswe_ctx* c, Full3 U, bool with_b, cudaStream_t st) {
+  const double2* b = c->bfull.p;
+  const int nf = (with_b && b) ? 4 : 3;
+  TRY(c->hout.alloc((size_t)8 * 4));
+  herm_full_kernel<1024><<<nf, 1024, 0, st>>>(c->nx, c->ny, U.u, U.v, U.e, b, c->hout.p);
+  c->launches++;
+  c->variant[PSWE_V_HERM]++;
+  CU(cudaGetLastError());
+  double h[32];
+  CU(cudaMemcpyAsync(h, c->hout.p, (size_t)8 * nf * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  const double vel = std::max(h[0], h[8]);
+  for (int f = 0; f < nf; ++f) {
+    const double* o = h + 8 * f;
+    if (o[7] != 0.0) continue;  // non-finite field: left to the callers' finite checks
+    const double ref = f < 2 ? std::max(o[0], vel) : o[0];
+    if (ref > 0.0 && o[1] > 1e-12 * ref) {
+      std::string m;
+      herm_message(c, o[1], ref, (long long)o[2], &m);
+      return set_err(PSWE_EHERM, "%s", m.c_str());
+    }
+  }
   return PSWE_OK;
 }
 
@@ -596,31 +703,38 @@ Full3 f3(const double* u, const double* v, const double* e) {
 Full3w f3w(double* u, double* v, double* e) { return Full3w{(double2*)u, (double2*)v, (double2*)e}; }
 Full3 f3c(const Full3w& a) { return Full3{a.u, a.v, a.e}; }
 
+// flags word: bit 3 (stage - 1) + field = non-finite field after a stage;
+// bit HERM_BIT0 + stage - 1 = the gate flagged that stage's RHS input;
+// HERM_BIT_RHS = the gate flagged a standalone evaluation's input
+constexpr int HERM_BIT0 = 9, HERM_BIT_RHS = 12;
+
 int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
   const size_t n = c->full_elems();
   TRY(ensure_compact(c));
-  TRY(c->full_tmp.alloc(n * 15));
+  TRY(c->full_tmp.alloc(n * 18));
   Full3w edt{c->full_tmp.p, c->full_tmp.p + n, c->full_tmp.p + 2 * n};
   Full3w u1{c->full_tmp.p + 3 * n, c->full_tmp.p + 4 * n, c->full_tmp.p + 5 * n};
   Full3w u2{c->full_tmp.p + 6 * n, c->full_tmp.p + 7 * n, c->full_tmp.p + 8 * n};
   const GridDev G = c->grid();
   const Prop pr = c->prop();
   const int P = (int)c->s_live.size();
+  TRY(ensure_hgate(c, P));
   const int gb = elem_grid(c, n);
   // stage 1
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, U.u, U.v, U.e, c->Uc.p));
+  CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, U.u, U.v, U.e, c->Uc.p,
+              c->hgate.p));
   c->launches++;
-  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
+  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st, HERM_BIT0));
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)c->Ac.p, edt, u1, c->flags.p));
   c->launches++;
   // stage 2
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, (const double2*)u1.u,
-              (const double2*)u1.v, (const double2*)u1.e, c->Uc.p));
+              (const double2*)u1.v, (const double2*)u1.e, c->Uc.p, c->hgate.p));
   c->launches++;
-  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
+  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st, HERM_BIT0 + 1));
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage2_kernel, gb, 256, 0, st, G, pr, dt, U, f3c(u1), (const double2*)c->Ac.p, u2,
               c->flags.p));
@@ -628,9 +742,9 @@ int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
   // stage 3
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, (const double2*)u2.u,
-              (const double2*)u2.v, (const double2*)u2.e, c->Uc.p));
+              (const double2*)u2.v, (const double2*)u2.e, c->Uc.p, c->hgate.p));
   c->launches++;
-  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st));
+  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st, HERM_BIT0 + 2));
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage3_kernel, gb, 256, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)c->Ac.p, out,
               c->flags.p));
@@ -651,6 +765,36 @@ int decode_flags(int bits, int* stage, int* field) {
 }
 
 const char* field_name(int f) { return f == 0 ? "u" : (f == 1 ? "v" : "eta"); }
+
+// The step's flags in the reference's order of events (integrator.py:95-102):
+// stage s's RHS input through the gate, then stage s's finite check.
+// `in` is the step's input state; the stage 2 / 3 inputs are the stepper's
+// u1 / u2 scratch.  Returns PSWE_OK, PSWE_EHERM (message set) or
+// PSWE_ENONFINITE (message, *stage and *field set).
+int step_verdict(pswe_ctx* c, int bits, Full3 in, cudaStream_t st, int* stage, int* field) {
+  const size_t n = c->full_elems();
+  const double2* t = c->full_tmp.p;
+  const Full3 inputs[3] = {in, {t + 3 * n, t + 4 * n, t + 5 * n}, {t + 6 * n, t + 7 * n, t + 8 * n}};
+  for (int sg = 1; sg <= 3; ++sg) {
+    if (bits & (1 << (HERM_BIT0 + sg - 1))) {
+      const int rc = exact_gate(c, c->s_dev.p, c->s_live, &c->k_live, inputs[sg - 1], st);
+      if (rc != PSWE_OK) {
+        *stage = sg;
+        *field = -1;
+        return rc;
+      }
+    }
+    for (int fl = 0; fl < 3; ++fl)
+      if (bits & (1 << (3 * (sg - 1) + fl))) {
+        *stage = sg;
+        *field = fl;
+        return set_err(PSWE_ENONFINITE, "non-finite values in field %s after stage %d", field_name(fl), sg);
+      }
+  }
+  *stage = 0;
+  *field = -1;
+  return PSWE_OK;
+}
 
 // Capture "step A -> B, copy B -> A" as a CUDA graph (cached per dt and
 // configuration version).  Every buffer it touches is allocated by the
@@ -836,11 +980,20 @@ int pswe_set_topography(pswe_ctx* c, const double* b_dev, void* stream) {
   TRY(c->Uc.alloc(c->compact_elems()));
   const GridDev G = c->grid();
   const double2* b = (const double2*)b_dev;
-  pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p);
+  // b's own Hermitian defect enters the gate's bound (herm_eval_kernel)
+  TRY(ensure_hgate(c, 1));
+  double* bstat = c->hgate.p + 1;  // scratch slots 1..3 (the statistic of field 0 lands in slot 1)
+  CU(cudaMemsetAsync(bstat, 0, 3 * sizeof(double), st));
+  pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p, bstat);
   c->launches++;
   CU(cudaMemcpyAsync(c->bc.p, c->Uc.p, (size_t)c->Ky * c->Kx * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   TRY(c->bfull.alloc(c->full_elems()));
   CU(cudaMemcpyAsync(c->bfull.p, b, c->full_elems() * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  double d2 = 0.0;
+  CU(cudaMemcpyAsync(&d2, bstat, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemsetAsync(c->hgate.p, 0, 4 * sizeof(double), st));
+  CU(cudaStreamSynchronize(st));
+  c->bdef = std::sqrt(d2);
   c->version++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -916,7 +1069,7 @@ int pswe_pack(pswe_ctx* c, const double* u, const double* v, const double* e, do
   if (!c || !u || !v || !e || !Uc) return set_err(PSWE_EINVAL, "null argument");
   CU(cudaSetDevice(c->device));
   pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, (cudaStream_t)stream>>>(
-      c->grid(), (const double2*)u, (const double2*)v, (const double2*)e, (double2*)Uc);
+      c->grid(), (const double2*)u, (const double2*)v, (const double2*)e, (double2*)Uc, nullptr);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -941,26 +1094,41 @@ int pswe_averaged_tendency_compact(pswe_ctx* c, const double* Uc, double* Ac, vo
                      (cudaStream_t)stream);
 }
 
+// full layout in, with the gate: pack (+ statistics), evaluation over the
+// nodes (s_dev, P) with the gate's verdict, unpack, synchronise, and the
+// exact check when flagged (node-wrapped message when `k` is given)
+static int gated_rhs(pswe_ctx* c, const double* u, const double* v, const double* e, double* du, double* dv,
+                     double* de, const double* s_dev, const double* w_dev, const std::vector<double>& s_host,
+                     const std::vector<int>* k, cudaStream_t st) {
+  CU(cudaSetDevice(c->device));
+  TRY(ensure_compact(c));
+  const int P = (int)s_host.size();
+  TRY(ensure_hgate(c, P));
+  CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
+  pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, st>>>(c->grid(), (const double2*)u, (const double2*)v,
+                                                               (const double2*)e, c->Uc.p, c->hgate.p);
+  c->launches++;
+  CU(cudaGetLastError());
+  TRY(rhs_compact(c, s_dev, w_dev, P, c->Uc.p, c->Ac.p, st, HERM_BIT_RHS));
+  TRY(pswe_unpack(c, (const double*)c->Ac.p, du, dv, de, st));
+  CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (*c->flags_host & (1 << HERM_BIT_RHS)) return exact_gate(c, s_dev, s_host, k, f3(u, v, e), st);
+  return PSWE_OK;
+}
+
 int pswe_averaged_tendency(pswe_ctx* c, const double* u, const double* v, const double* e, double* du,
                            double* dv, double* de, void* stream) {
   if (!c || !u || !v || !e || !du || !dv || !de) return set_err(PSWE_EINVAL, "null argument");
   if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
   TRY(check_nodes(c));
-  CU(cudaSetDevice(c->device));
-  TRY(ensure_compact(c));
-  TRY(pswe_pack(c, u, v, e, (double*)c->Uc.p, stream));
-  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, (int)c->s_live.size(), c->Uc.p, c->Ac.p, (cudaStream_t)stream));
-  return pswe_unpack(c, (const double*)c->Ac.p, du, dv, de, stream);
+  return gated_rhs(c, u, v, e, du, dv, de, c->s_dev.p, c->w_dev.p, c->s_live, &c->k_live, (cudaStream_t)stream);
 }
 
 int pswe_apply_nonlinear(pswe_ctx* c, const double* u, const double* v, const double* e, double* du, double* dv,
                          double* de, void* stream) {
   if (!c || !u || !v || !e || !du || !dv || !de) return set_err(PSWE_EINVAL, "null argument");
-  CU(cudaSetDevice(c->device));
-  TRY(ensure_compact(c));
-  TRY(pswe_pack(c, u, v, e, (double*)c->Uc.p, stream));
-  TRY(rhs_compact(c, c->zero_s.p, c->one_w.p, 1, c->Uc.p, c->Ac.p, (cudaStream_t)stream));
-  return pswe_unpack(c, (const double*)c->Ac.p, du, dv, de, stream);
+  return gated_rhs(c, u, v, e, du, dv, de, c->zero_s.p, c->one_w.p, c->zero_live, nullptr, (cudaStream_t)stream);
 }
 
 int pswe_apply_linear(pswe_ctx* c, const double* u, const double* v, const double* e, double* lu, double* lv,
@@ -997,19 +1165,26 @@ int pswe_ssprk3_step(pswe_ctx* c, double dt, const double* u, const double* v, c
   TRY(check_nodes(c));
   CU(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  const size_t n = c->full_elems();
+  TRY(c->full_tmp.alloc(n * 18));
+  Full3 in = f3(u, v, e);
+  if (ou == u || ov == v || oe == e || ou == v || ou == e || ov == u || ov == e || oe == u || oe == v) {
+    // in place: keep the input for the gate's exact check (the output overwrites it)
+    double2* keep = c->full_tmp.p + 9 * n;
+    CU(cudaMemcpyAsync(keep, u, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(keep + n, v, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(keep + 2 * n, e, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    in = Full3{keep, keep + n, keep + 2 * n};
+  }
   CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
-  TRY(step_impl(c, dt, f3(u, v, e), f3w(ou, ov, oe), st));
+  TRY(step_impl(c, dt, in, f3w(ou, ov, oe), st));
   CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   int stage = 0, field = -1;
-  if (decode_flags(*c->flags_host, &stage, &field)) {
-    if (bad_stage) *bad_stage = stage;
-    if (bad_field) *bad_field = field;
-    return set_err(PSWE_ENONFINITE, "non-finite values in field %s after stage %d", field_name(field), stage);
-  }
-  if (bad_stage) *bad_stage = 0;
-  if (bad_field) *bad_field = -1;
-  return PSWE_OK;
+  const int rc = *c->flags_host ? step_verdict(c, *c->flags_host, in, st, &stage, &field) : PSWE_OK;
+  if (bad_stage) *bad_stage = stage;
+  if (bad_field) *bad_field = field;
+  return rc;
 }
 
 int pswe_run(pswe_ctx* c, double dt, int nsteps, double* u, double* v, double* e, int* bad_step, int* bad_stage,
@@ -1042,20 +1217,25 @@ int pswe_run(pswe_ctx* c, double dt, int nsteps, double* u, double* v, double* e
   const Full3 Ain{A, A + n, A + 2 * n};
   const Full3w Bout{B, B + n, B + 2 * n};
 
-  // one checked step: A -> B -> A; returns 100 (and fills the outputs) on a non-finite stage
+  // one checked step: A -> B -> A; returns 100 (and fills the outputs) when
+  // the step fails (non-finite stage or the Hermitian gate)
   int rc = PSWE_OK;
   auto checked_step = [&](int i) -> int {
     CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
     TRY(step_impl(c, dt, Ain, Bout, st));
     CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    int stage = 0, field = -1;
-    if (decode_flags(*c->flags_host, &stage, &field)) {
-      if (bad_step) *bad_step = i;
-      if (bad_stage) *bad_stage = stage;
-      if (bad_field) *bad_field = field;
-      rc = set_err(PSWE_ENONFINITE, "non-finite values in field %s after stage %d", field_name(field), stage);
-      return 100;  // A still holds the state at the start of step i
+    if (*c->flags_host) {
+      int stage = 0, field = -1;
+      const int r = step_verdict(c, *c->flags_host, Ain, st, &stage, &field);
+      if (r == PSWE_ENONFINITE || r == PSWE_EHERM) {
+        if (bad_step) *bad_step = i;
+        if (bad_stage) *bad_stage = stage;
+        if (bad_field) *bad_field = field;
+        rc = r;
+        return 100;  // A still holds the state at the start of step i
+      }
+      if (r != PSWE_OK) return r;
     }
     CU(cudaMemcpyAsync(A, B, bytes3, cudaMemcpyDeviceToDevice, st));
     return 0;
@@ -1154,6 +1334,7 @@ int pswe_to_physical(pswe_ctx* c, const double* u, const double* v, const double
                                 void* stream) {
   if (!c || !u || !v || !e || !phys) return set_err(PSWE_EINVAL, "null argument");
   CU(cudaSetDevice(c->device));
+  TRY(full_gate(c, f3(u, v, e), false, (cudaStream_t)stream));
   return physical_fields(c, u, v, e, phys, (cudaStream_t)stream);
 }
 
@@ -1184,6 +1365,7 @@ int pswe_diagnostics(pswe_ctx* c, const double* u, const double* v, const double
   if (!c || !u || !v || !e || !out3) return set_err(PSWE_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   CU(cudaSetDevice(c->device));
+  TRY(full_gate(c, f3(u, v, e), true, st));
   TRY(physical_fields(c, u, v, e, nullptr, st));
   std::vector<double> part((size_t)3 * c->nx);
   CU(cudaMemcpyAsync(part.data(), c->diag_part.p, part.size() * sizeof(double), cudaMemcpyDeviceToHost, st));

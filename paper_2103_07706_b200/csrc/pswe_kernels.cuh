@@ -47,6 +47,11 @@ struct GridDev {
   const double2* bc;   // [Ky][Kx] compact (Hermitian-projected) topography
 };
 
+__device__ __forceinline__ double abs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+// max that propagates NaN (either operand) -- the Hermitian gate's statistics
+// must not drop a non-finite value the way fmax does
+__device__ __forceinline__ double nanmax(double a, double b) { return (a > b || a != a) ? a : b; }
+
 struct PhaseDev {
   const double* s;  // [P] live node shifts, ascending k
   const double* w;  // [P] weights
@@ -139,7 +144,7 @@ struct PassAW {
 template <int NX>
 __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
     passA_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, const double2* __restrict__ Uc,
-                 const double2* __restrict__ ctab, double2* __restrict__ I) {
+                 const double2* __restrict__ ctab, double2* __restrict__ I, double* __restrict__ pscale) {
   griddep_wait();
   griddep_launch();
   using W = PassAW<NX>;
@@ -196,6 +201,8 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
     double kyb[GPW];
 #pragma unroll
     for (int c = 0; c < GPW; ++c) kyb[c] = G.kyc[min(j0 + c, Ky - 1)];
+    // Hermitian gate (pscale): max squared magnitude of u', v', eta' - b per phase
+    double gmax0 = 0.0, gmax1 = 0.0;
     for (int idx = threadIdx.x; idx < ncol * Kx; idx += blockDim.x) {
       const int tt = idx / Kx, r = idx % Kx;
       double2* e = buf + idx;
@@ -212,9 +219,27 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
         C3 q = tab ? exp_c12(sub ? cb : e[4 * fs], q0, G.ph, kx, ky)
                    : expL(ph.s[p0 + pa + sub], q0, G.ph, kx, ky, pr);
         double2* o = e + (size_t)(3 * sub) * fs;
+        const double2 dep = csub(q.e, bb);
         o[0] = cscale(G.inv_n2, q.u);
         o[fs] = cscale(G.inv_n2, q.v);
-        o[2 * fs] = cscale(G.inv_n2, csub(q.e, bb));
+        o[2 * fs] = cscale(G.inv_n2, dep);
+        if (pscale) {
+          const double m = nanmax(nanmax(abs2(q.u), abs2(q.v)), abs2(dep));
+          if (sub) gmax1 = nanmax(m, gmax1);
+          else gmax0 = nanmax(m, gmax0);
+        }
+      }
+    }
+    if (pscale) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        gmax0 = nanmax(gmax0, __shfl_xor_sync(0xffffffffu, gmax0, o));
+        gmax1 = nanmax(gmax1, __shfl_xor_sync(0xffffffffu, gmax1, o));
+      }
+      if (lane == 0) {
+        unsigned long long* ps = reinterpret_cast<unsigned long long*>(pscale + p0 + pa);
+        atomicMax(ps, (unsigned long long)__double_as_longlong(gmax0));
+        if (hasq) atomicMax(ps + 1, (unsigned long long)__double_as_longlong(gmax1));
       }
     }
     fence_proxy_async();  // order these stores before the next block's TMA refill of buf
@@ -988,12 +1013,15 @@ __global__ void reduce_slots_kernel(const double2* __restrict__ slots, int Gc, s
 // layout conversion full <-> compact
 // ============================================================================
 // pack with Hermitian projection (c(k) + conj c(-k))/2, which is what the
-// reference's real(ifft2(.)) does to a field (grid.py:173-174).
+// reference's real(ifft2(.)) does to a field (grid.py:173-174).  With hstat,
+// also the Hermitian gate's statistic: hstat[f] = max over the band of
+// |c(k) - conj c(-k)|^2 per field (herm_kernels.cuh; NaN propagates).
 __global__ void pack_kernel(GridDev G, const double2* __restrict__ u, const double2* __restrict__ v,
-                            const double2* __restrict__ e, double2* __restrict__ Uc) {
+                            const double2* __restrict__ e, double2* __restrict__ Uc, double* __restrict__ hstat) {
   griddep_wait();
   griddep_launch();
   const size_t KyKx = (size_t)G.Ky * G.Kx;
+  double dmax[3] = {0.0, 0.0, 0.0};
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 3 * KyKx; i += (size_t)gridDim.x * blockDim.x) {
     const int f = (int)(i / KyKx);
     const int rem = (int)(i % KyKx);
@@ -1005,6 +1033,21 @@ __global__ void pack_kernel(GridDev G, const double2* __restrict__ u, const doub
     const double2 a = c[(size_t)ix * G.ny + jy];
     const double2 b = c[(size_t)jx * G.ny + my];
     Uc[i] = cmk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+    if (hstat) {
+      const double dx = a.x - b.x, dy = a.y + b.y;
+      const double d2 = fma(dx, dx, dy * dy);
+      dmax[f] = nanmax(d2, dmax[f]);
+    }
+  }
+  if (hstat) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      double m = dmax[f];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0 && m != 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(hstat + f), (unsigned long long)__double_as_longlong(m));
+    }
   }
 }
 

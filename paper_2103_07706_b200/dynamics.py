@@ -123,11 +123,11 @@ def upload(ctx, state, band: bool = False):
     return _native.upload_fields(fields, ctx.device, band_ctx=ctx if band else None)
 
 
-def download(tensors, band_ctx=None):
+def download(tensors, band_ctx=None, hosts=None):
     """Device tensors -> numpy.  ``band_ctx``: the tensors vanish outside the
     2/3 band (a dealiased tendency), so only the band is copied back."""
     if tensors and tensors[0].is_cuda:
-        return _native.download_fields(tensors, band_ctx=band_ctx)
+        return _native.download_fields(tensors, band_ctx=band_ctx, hosts=hosts)
     return [t.numpy() for t in tensors]
 
 
@@ -145,9 +145,12 @@ def apply_linear(state, params):
 
 
 def apply_nonlinear(state, params):
-    """N(U) on the GPU (dynamics.py:139-176): fused pseudo-spectral passes, 2/3-dealiased."""
+    """N(U) on the GPU (dynamics.py:139-176): fused pseudo-spectral passes,
+    2/3-dealiased; the input passes the Hermitian gate of to_physical
+    (grid.py:159-172) or ValueError names its worst mode."""
     ctx = context(state, params)
-    return rebuild(state, download(ctx.apply_nonlinear(upload(ctx, state))), state.t)
+    U = upload(ctx, state, band=True)
+    return rebuild(state, download(ctx.apply_nonlinear(U), band_ctx=ctx), state.t)
 
 
 def dispersion_omega(kappa, params) -> np.ndarray:

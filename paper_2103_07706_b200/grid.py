@@ -88,10 +88,40 @@ def to_spectral(grid: SpectralGrid, phys) -> np.ndarray:
     return np.fft.fft2(phys.astype(np.float64, copy=False))
 
 
+HERMITIAN_RTOL = 1e-12  # grid.py:31
+
+
+def hermitian_defect(c: np.ndarray) -> np.ndarray:
+    """|c(k) - conj c(-k)| per mode (the mirror index is -i mod n)."""
+    mirror = np.roll(c[::-1, ::-1], 1, axis=(0, 1))
+    return np.abs(c - np.conj(mirror))
+
+
+def hermitian_gate(grid: SpectralGrid, c: np.ndarray, scale=None) -> None:
+    """The reference's symmetry gate (grid.py:159-172): ValueError naming the
+    worst mode when the defect exceeds HERMITIAN_RTOL relative to
+    max(max|c|, scale).  The device paths apply the same gate in CUDA
+    (herm_kernels.cuh); this host copy serves the host-side diagnostics."""
+    ref = float(np.max(np.abs(c)))
+    if scale is not None:
+        ref = max(ref, float(scale))
+    if not ref > 0.0:
+        return
+    d = hermitian_defect(c)
+    worst = float(d.max())
+    if worst > HERMITIAN_RTOL * ref:
+        i, j = np.unravel_index(int(np.argmax(d)), d.shape)
+        wx, wy = int(_signed_index(grid.nx)[i]), int(_signed_index(grid.ny)[j])
+        raise ValueError(f"non-Hermitian spectral field: mode (kx index {wx}, ky index {wy}) has asymmetry "
+                         f"{worst:.3e} (relative {worst / ref:.3e})")
+
+
 def to_physical(grid: SpectralGrid, coeffs, scale=None) -> np.ndarray:
-    """Host real(ifft2) of Hermitian coefficients (grid.py:140-180 without the gate)."""
+    """Host real(ifft2) of Hermitian coefficients, behind the reference's
+    symmetry gate (grid.py:140-180)."""
     c = np.asarray(coeffs, dtype=np.complex128)
     _shape_check(grid, c, "spectral field")
+    hermitian_gate(grid, c, scale)
     return np.fft.ifft2(c).real
 
 

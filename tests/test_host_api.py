@@ -123,3 +123,35 @@ def test_case_c5_is_geostrophically_balanced():
         U = np.stack([c.state.u, c.state.v, c.state.eta])
         assert O.energy_norm(S, O.linear(S, U)) <= 1e-12 * p.f * O.energy_norm(S, U)
         assert c.P == 15 and math.isclose(float(np.max(np.abs(O.real_field(U[2])))), 0.1 * p.H, rel_tol=1e-12)
+
+
+def test_host_to_physical_gate_matches_reference():
+    """The host to_physical carries the reference's symmetry gate
+    (grid.py:159-172): same exception and message, same pass/fail edge."""
+    import numpy as np
+    from oracle import reference as R
+    from paper_2103_07706_b200 import grid as G
+
+    rng = np.random.default_rng(3)
+    g = G.make_grid(12, 16, 3.0e6, 4.0e6)
+    c = np.fft.fft2(rng.standard_normal((12, 16)))
+    G.to_physical(g, c)  # round-off asymmetry passes
+    ref = R.load()
+    for i, j, rel in ((2, 3, 1e-6), (0, 5, 1e-9), (7, 0, 2e-12), (6, 8, 1e-3)):
+        bad = c.copy()
+        bad[i, j] += rel * np.max(np.abs(c))
+        try:
+            G.to_physical(g, bad, scale=None)
+            ours = None
+        except ValueError as exc:
+            ours = str(exc)
+        assert ours is None or ours.startswith("non-Hermitian spectral field: mode (kx index ")
+        if ref is not None:
+            from phaseswe import grid as RG
+            rg = RG.make_grid(12, 16, 3.0e6, 4.0e6)
+            try:
+                RG.to_physical(rg, bad)
+                want = None
+            except ValueError as exc:
+                want = str(exc)
+            assert ours == want, (ours, want)
