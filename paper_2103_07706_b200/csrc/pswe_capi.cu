@@ -539,8 +539,11 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   c->pdl = pdl_enabled() && nchunks == 1;
   TRY(c->inter.alloc(per_phase * CP * lanes));
   TRY(c->slots.alloc((size_t)lanes * Gc * c->compact_elems()));
-  if (getenv("PSWE_DEBUG_POISON")) {  // debug: NaN-fill intermediates to expose unwritten entries
+  static const bool poison = getenv("PSWE_DEBUG_POISON") != nullptr;
+  if (poison) {  // debug: NaN-fill every scratch and the output, exposing entries read before written
     CU(cudaMemsetAsync(c->inter.p, 0xFF, per_phase * CP * lanes * sizeof(double2), st));
+    CU(cudaMemsetAsync(c->slots.p, 0xFF, (size_t)lanes * Gc * c->compact_elems() * sizeof(double2), st));
+    CU(cudaMemsetAsync(Ac, 0xFF, c->compact_elems() * sizeof(double2), st));
   }
   PhaseDev ph{s, w, P};
   cudaStream_t lst[pswe_ctx::MAX_LANES] = {st, c->st_lane[0], c->st_lane[1], c->st_lane[2]};

@@ -30,15 +30,15 @@ def oracle_diag(state, params):
     return en, ms, float(speed)
 
 
-def random_state(nx, ny, seed):
-    """Full-spectrum (not band-limited) real fields, plus a non-Hermitian
-    perturbation that real(ifft2) must discard."""
+def random_state(nx, ny, seed, asym=0.0):
+    """Full-spectrum (not band-limited) real fields; `asym` adds a
+    non-Hermitian perturbation of that relative size."""
     rng = np.random.default_rng(seed)
     g = pk.make_grid(nx, ny, 4.0e7, 4.0e7 * ny / nx)
     fields = []
     for scale in (20.0, 15.0, 50.0):
         c = np.fft.fft2(scale * rng.standard_normal((nx, ny)))
-        c = c + 1e-3 * scale * (rng.standard_normal((nx, ny)) + 1j * rng.standard_normal((nx, ny)))
+        c = c + asym * scale * (rng.standard_normal((nx, ny)) + 1j * rng.standard_normal((nx, ny)))
         fields.append(c)
     return pk.State(grid=g, u=fields[0], v=fields[1], eta=fields[2], t=0.0)
 
@@ -48,6 +48,21 @@ def check(state, params):
     want = oracle_diag(state, params)
     for g, w in zip(got, want):
         assert abs(g - w) <= TOL * abs(w), (got, want)
+
+
+def test_diagnostics_gate_non_hermitian_input():
+    """The snapshot path's to_physical gate (diagnostics.py:21-25): a
+    non-Hermitian u fails with the host gate's (= the reference's) message;
+    a round-off-sized asymmetry (1e-15) passes."""
+    st = random_state(64, 32, seed=3, asym=1e-3)
+    params = pk.PhysicsParams(f=1.0e-4, g=9.81, H=5000.0, b=np.zeros((64, 32), complex))
+    vel = max(float(np.max(np.abs(st.u))), float(np.max(np.abs(st.v))))
+    with pytest.raises(ValueError) as want:
+        pk.to_physical(st.grid, st.u, vel)
+    with pytest.raises(ValueError) as got:
+        integrator.device_diagnostics(st, params)
+    assert str(got.value) == str(want.value)
+    check(random_state(64, 32, seed=3, asym=1e-15), params)
 
 
 @pytest.mark.parametrize("nx,ny", [(64, 64), (512, 512), (64, 32), (8, 16)])

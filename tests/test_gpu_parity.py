@@ -447,3 +447,54 @@ def test_single_node_large_grid_matches_oracle(level):
     assert O.rel_l2(arr(one), O.ssprk3_step(S, U, 180.0, [0.0], [1.0])) <= STEP_TOL
     v = pk.dynamics.context(st, c.params).variant_launches
     assert v["passB_split"] > 0
+
+
+def test_poisoned_scratch_gives_the_same_bits(tmp_path):
+    """Stand-in for compute-sanitizer's initcheck/racecheck (closed on the
+    GPU pool): with every intermediate, slot and the output NaN-filled before
+    each evaluation (PSWE_DEBUG_POISON), every kernel variant -- split,
+    row and paired pass B, one and four lanes, one and many chunks and pass-C
+    groups -- must produce the same bits as without, so no entry is read
+    before it is written and no read races its producer."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys, json, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2103_07706_b200 as pk\n"
+        "from paper_2103_07706_b200 import cases\n"
+        "outs, var = [], {}\n"
+        "for r, M in ((3, 256), (4, 8), (5, 32), (6, 128), (7, 8), (7, 64)):\n"
+        "    c = cases.case_c5(r, M)\n"
+        "    ctx = pk.dynamics.context(c.state, c.params)\n"
+        "    ctx.set_propagator('exact')\n"
+        "    ctx.set_quadrature(c.quadrature.s, c.quadrature.w)\n"
+        "    Uc = ctx.pack(pk.dynamics.upload(ctx, c.state))\n"
+        "    for _ in range(3):\n"
+        "        outs.append(ctx.averaged_tendency_compact(Uc).cpu().numpy())\n"
+        "    for k, v in ctx.variant_launches.items(): var[k] = var.get(k, 0) + v\n"
+        "c = cases.case_c2()\n"
+        "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
+        "s = pk.run(c.state, cfg, c.params, t_end=4 * c.dt).states[-1]\n"
+        "outs.append(np.stack([s.u, s.v, s.eta]))\n"
+        "np.savez(sys.argv[1], *outs)\n"
+        "print(json.dumps(var))\n" % str(ROOT))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
+    res = []
+    for i, env in enumerate(({}, {"PSWE_DEBUG_POISON": "1"})):
+        f = tmp_path / f"p{i}.npz"
+        p = subprocess.run([sys.executable, "-c", code, str(f)], env={**base, **env},
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr
+        var = json.loads(p.stdout.strip().splitlines()[-1])
+        with np.load(f) as z:
+            res.append([z[k] for k in z.files])
+    for name in ("passB_split", "passB_row", "passB_pair", "reduce"):
+        assert var[name] > 0, (name, var)
+    for a, b in zip(res[0], res[1]):
+        assert np.all(np.isfinite(b))
+        assert np.array_equal(a, b)
