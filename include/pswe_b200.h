@@ -124,6 +124,28 @@ int pswe_ssprk3_step(pswe_ctx* ctx, double dt, const double* u_dev, const double
 int pswe_run(pswe_ctx* ctx, double dt, int nsteps, double* u_dev, double* v_dev, double* eta_dev,
              int* bad_step, int* bad_stage, int* bad_field, void* stream);
 
+/* Window batch (the window sweep, harness.py:110-147 cmd_sweep and
+ * validation.py:251-271): W averaging windows -- each its own quadrature of
+ * n_nodes[i] = 2 M_i + 1 nodes, s and w concatenated over the windows in
+ * window order -- advanced together: one launch sequence per stage serves
+ * every window, the phases of all windows forming one batch axis
+ * (window, phase).  Zero-weight nodes are skipped as in
+ * pswe_set_quadrature.  Grid, physics, topography and propagator are the
+ * context's. */
+int pswe_set_window_batch(pswe_ctx* ctx, int W, const int* n_nodes, const double* s_host, const double* w_host);
+
+/* Averaged tendencies of the W windows: Uc / Ac = W compact states
+ * ([W][3][Ky][Kx]); window w's tendency uses window w's state and nodes. */
+int pswe_window_batch_tendency(pswe_ctx* ctx, const double* Uc_dev, double* Ac_dev, void* stream);
+
+/* nsteps transformed SSPRK3 steps of all W windows in place on
+ * U_dev = [W][3][nx][ny] (window w's u, v, eta).  When any window's step
+ * flags a non-finite stage or the Hermitian gate, returns PSWE_ENONFINITE
+ * with *bad_step (1-based) and every window left at the start of that step;
+ * the caller replays the windows one by one (pswe_run) for the reference's
+ * per-window error. */
+int pswe_window_batch_run(pswe_ctx* ctx, double dt, int nsteps, double* U_dev, int* bad_step, void* stream);
+
 /* Largest |eigenvalue| of L over the grid (max_frequency, dynamics.py:189-192). */
 double pswe_max_frequency(const pswe_ctx* ctx);
 

@@ -54,6 +54,9 @@ SIGNATURES = {
     "pswe_propagate": (_i, [_vp, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_ssprk3_step": (_i, [_vp, _d, _vp, _vp, _vp, _vp, _vp, _vp, _c_int_p, _c_int_p, _vp]),
     "pswe_run": (_i, [_vp, _d, _i, _vp, _vp, _vp, _c_int_p, _c_int_p, _c_int_p, _vp]),
+    "pswe_set_window_batch": (_i, [_vp, _i, _c_int_p, ctypes.POINTER(_d), ctypes.POINTER(_d)]),
+    "pswe_window_batch_tendency": (_i, [_vp, _vp, _vp, _vp]),
+    "pswe_window_batch_run": (_i, [_vp, _d, _i, _vp, _c_int_p, _vp]),
     "pswe_max_frequency": (_d, [_vp]),
     "pswe_launch_count": (ctypes.c_int64, [_vp]),
     "pswe_variant_launches": (_i, [_vp, ctypes.POINTER(ctypes.c_int64), _i]),
@@ -479,6 +482,34 @@ class Context:
             return out, (st.value, fl.value)
         _check(rc)
         return out, (0, -1)
+
+    # ---- window batch ----------------------------------------------------
+    def set_window_batch(self, quads) -> None:
+        """W quadratures (objects with .s, .w) as one window batch."""
+        n = np.array([len(q.s) for q in quads], dtype=np.int32)
+        s = np.ascontiguousarray(np.concatenate([np.asarray(q.s, dtype=np.float64) for q in quads]))
+        w = np.ascontiguousarray(np.concatenate([np.asarray(q.w, dtype=np.float64) for q in quads]))
+        dp = ctypes.POINTER(ctypes.c_double)
+        _check(_lib.pswe_set_window_batch(self.h, len(quads), n.ctypes.data_as(_c_int_p), s.ctypes.data_as(dp),
+                                          w.ctypes.data_as(dp)))
+        self.batch_windows = len(quads)
+
+    def window_batch_tendency(self, Uc, out=None):
+        """(W, 3, Ky, Kx) compact states -> their averaged tendencies."""
+        out = self.torch.empty_like(Uc) if out is None else out
+        _check(_lib.pswe_window_batch_tendency(self.h, _dptr(Uc), _dptr(out), _stream(self.torch)))
+        return out
+
+    def window_batch_run(self, dt: float, nsteps: int, U) -> int:
+        """In place on U = (W, 3, nx, ny) complex128; returns 0 or the first
+        flagged step (all windows then stand at its start)."""
+        bs = ctypes.c_int(0)
+        rc = _lib.pswe_window_batch_run(self.h, float(dt), int(nsteps), _dptr(U), ctypes.byref(bs),
+                                        _stream(self.torch))
+        if rc == PSWE_ENONFINITE:
+            return bs.value
+        _check(rc)
+        return 0
 
     def diagnostics(self, U) -> tuple[float, float, float]:
         """(energy, mass, max speed) of a full-layout state on the device."""

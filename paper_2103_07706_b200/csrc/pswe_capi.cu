@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <cmath>
 #include <cstdarg>
@@ -57,6 +58,10 @@ bool pow2_ok(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
 // those calls are serialised process-wide.
 std::recursive_mutex g_capture_mutex;
 
+// bumped by every device (re)allocation: a captured graph whose buffers may
+// have moved is re-captured
+std::atomic<int64_t> g_alloc_gen{0};
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -64,6 +69,7 @@ struct DevBuf {
   int alloc(size_t count) {
     if (count <= n) return PSWE_OK;
     std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
+    ++g_alloc_gen;
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
@@ -114,15 +120,28 @@ struct pswe_ctx {
   // cached CUDA graph of one SSPRK3 step (pswe_run)
   cudaGraphExec_t step_exec = nullptr;
   double graph_dt = 0.0;
-  int64_t version = 0, graph_version = -1, step_graph_launches = 0;
+  int64_t version = 0, graph_version = -1, step_graph_launches = 0, graph_gen = -1;
   const double2* graph_A = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t st_run = nullptr;  // pswe_run's stream (graph capture)
   cudaEvent_t ev_run = nullptr;
   // phase tables (c1, c2)[p][j][r] of the exact route: one for the quadrature,
-  // one for the single s = 0 node of apply_nonlinear; rebuilt when stale
-  DevBuf<double2> ctab_q, ctab_0;
-  bool ctab_q_valid = false, ctab_0_valid = false;
+  // one for the single s = 0 node of apply_nonlinear, one for the window
+  // batch; rebuilt when stale
+  DevBuf<double2> ctab_q, ctab_0, ctab_b;
+  bool ctab_q_valid = false, ctab_0_valid = false, ctab_b_valid = false;
+  // window batch (pswe_set_window_batch): bW windows' live phases concatenated
+  int bW = 0;
+  std::vector<double> b_s, b_w;
+  std::vector<int> b_win, b_k;
+  DevBuf<double> bs_dev, bw_dev;
+  DevBuf<int> bwin_dev;
+  DevBuf<double2> b_full;          // batch run: edt, u1, u2, A, B, S (6 x W states)
+  DevBuf<double2> b_Uc, b_Ac;      // W compact states
+  cudaGraphExec_t bstep_exec = nullptr;
+  double bgraph_dt = 0.0;
+  int64_t bgraph_version = -1, bstep_graph_launches = 0, bgraph_gen = -1;
+  int64_t bgraph_variant[PSWE_NUM_VARIANTS] = {};
   const double2* ctab_cur = nullptr;
   DevBuf<double2> full_tmp;  // stepper: edt, u1, u2 (3 states) + run ping-pong (2 states)
   DevBuf<int> flags;
@@ -224,12 +243,12 @@ bool pdl_enabled() {
 }
 
 // ---------------------------------------------------------------- dispatch
-template <int NX>
+template <int NX, bool MW>
 int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, double* pscale,
             cudaStream_t st) {
-  using W = PassAW<NX>;
+  using W = PassAW<NX, MW>;
   const size_t smem = W::bytes(c->Kx);
-  auto kern = passA_kernel<NX>;
+  auto kern = passA_kernel<NX, MW>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int nblk = ((np + 1) / 2) * ((c->Ky + W::GPW - 1) / W::GPW);
   const int blocks = std::min(nblk, W::CTAS * c->sms);
@@ -324,7 +343,7 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
   // prologue and slot update.  Pick the Gc with the best wave efficiency.
   const int cols = (c->Ky + PassCW<NX>::GPW - 1) / PassCW<NX>::GPW;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, passC_kernel<NX>, PassCW<NX>::WARPS * 32,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, passC_kernel<NX, false>, PassCW<NX>::WARPS * 32,
                                                     PassCW<NX>::bytes(c->Kx)) != cudaSuccess ||
       per_sm < 1)
     per_sm = 3;
@@ -348,12 +367,12 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
   return std::max(1, std::min(best, CP));
 }
 
-template <int NX>
+template <int NX, bool MW>
 int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
             double2* slots, cudaStream_t st) {
   using W = PassCW<NX>;
   const size_t smem = W::bytes(c->Kx);
-  auto kern = passC_kernel<NX>;
+  auto kern = passC_kernel<NX, MW>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int cols = (c->Ky + W::GPW - 1) / W::GPW;
   const int blocks = cols * Gc;
@@ -366,18 +385,24 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   return PSWE_OK;
 }
 
-int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, double* pscale,
-              cudaStream_t st) {
+template <bool MW>
+int dispatchA_(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, double* pscale,
+               cudaStream_t st) {
   switch (c->nx) {
-    case 8: return launchA<8>(c, ph, p0, np, Uc, I1, pscale, st);
-    case 16: return launchA<16>(c, ph, p0, np, Uc, I1, pscale, st);
-    case 32: return launchA<32>(c, ph, p0, np, Uc, I1, pscale, st);
-    case 64: return launchA<64>(c, ph, p0, np, Uc, I1, pscale, st);
-    case 128: return launchA<128>(c, ph, p0, np, Uc, I1, pscale, st);
-    case 256: return launchA<256>(c, ph, p0, np, Uc, I1, pscale, st);
-    case 512: return launchA<512>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 8: return launchA<8, MW>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 16: return launchA<16, MW>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 32: return launchA<32, MW>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 64: return launchA<64, MW>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 128: return launchA<128, MW>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 256: return launchA<256, MW>(c, ph, p0, np, Uc, I1, pscale, st);
+    case 512: return launchA<512, MW>(c, ph, p0, np, Uc, I1, pscale, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
+}
+int dispatchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, double2* I1, double* pscale,
+              cudaStream_t st) {
+  return ph.win ? dispatchA_<true>(c, ph, p0, np, Uc, I1, pscale, st)
+                : dispatchA_<false>(c, ph, p0, np, Uc, I1, pscale, st);
 }
 int dispatchB(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUtensorMap& mO, double2* I2,
               cudaStream_t st) {
@@ -404,18 +429,24 @@ int groupsC(const pswe_ctx* c, int CP) {
   }
 }
 
-int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
-              double2* slots, cudaStream_t st) {
+template <bool MW>
+int dispatchC_(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
+               double2* slots, cudaStream_t st) {
   switch (c->nx) {
-    case 8: return launchC<8>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 16: return launchC<16>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 32: return launchC<32>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 64: return launchC<64>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 128: return launchC<128>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 256: return launchC<256>(c, ph, p0, np, Gc, first, I2, slots, st);
-    case 512: return launchC<512>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 8: return launchC<8, MW>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 16: return launchC<16, MW>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 32: return launchC<32, MW>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 64: return launchC<64, MW>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 128: return launchC<128, MW>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 256: return launchC<256, MW>(c, ph, p0, np, Gc, first, I2, slots, st);
+    case 512: return launchC<512, MW>(c, ph, p0, np, Gc, first, I2, slots, st);
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported nx = %d", c->nx);
+}
+int dispatchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* I2,
+              double2* slots, cudaStream_t st) {
+  return ph.win ? dispatchC_<true>(c, ph, p0, np, Gc, first, I2, slots, st)
+                : dispatchC_<false>(c, ph, p0, np, Gc, first, I2, slots, st);
 }
 
 template <int NX>
@@ -495,18 +526,39 @@ int ensure_hgate(pswe_ctx* c, int P) {
   return PSWE_OK;
 }
 
+// The phases of one evaluation: device (s, w) of the live nodes, the window
+// of each phase for a window batch (win, W windows), and the phase table
+// that caches their exact-route (c1, c2) columns.
+struct PhaseSet {
+  const double* s;
+  const double* w;
+  const int* win;
+  int P, W;
+  DevBuf<double2>* tab;
+  bool* tab_valid;
+};
+PhaseSet quad_phases(pswe_ctx* c) {
+  return {c->s_dev.p, c->w_dev.p, nullptr, (int)c->s_live.size(), 1, &c->ctab_q, &c->ctab_q_valid};
+}
+PhaseSet zero_phases(pswe_ctx* c) { return {c->zero_s.p, c->one_w.p, nullptr, 1, 1, &c->ctab_0, &c->ctab_0_valid}; }
+PhaseSet batch_phases(pswe_ctx* c) {
+  return {c->bs_dev.p, c->bw_dev.p, c->bwin_dev.p, (int)c->b_s.size(), c->bW, &c->ctab_b, &c->ctab_b_valid};
+}
+
 // `gate_bit` >= 0: the input was packed with the gate's statistics
 // (pack_kernel hstat = hgate); pass A adds the per-phase scales and the
 // evaluation ends with herm_eval_kernel, which sets flags bit gate_bit when
-// the exact check has to decide.
-int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const double2* Uc, double2* Ac,
-                cudaStream_t st, int gate_bit = -1) {
+// the exact check has to decide.  A window batch (ps.win) evaluates W
+// windows' tendencies at once: Uc / Ac hold W compact states.
+int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac, cudaStream_t st,
+                int gate_bit = -1) {
+  const double* s = ps.s;
+  const int P = ps.P;
   // exact route: phase table (built once per quadrature / grid)
   c->ctab_cur = nullptr;
   if (c->kind == 0) {
-    const bool q = (s == c->s_dev.p);
-    DevBuf<double2>& tb = q ? c->ctab_q : c->ctab_0;
-    bool& valid = q ? c->ctab_q_valid : c->ctab_0_valid;
+    DevBuf<double2>& tb = *ps.tab;
+    bool& valid = *ps.tab_valid;
     if (!valid) {
       TRY(tb.alloc((size_t)P * c->Ky * c->Kx));
       phase_table_kernel<<<elem_grid(c, (size_t)P * c->Ky * c->Kx), 256, 0, st>>>(c->grid(), s, P, tb.p);
@@ -537,15 +589,22 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
   nchunks = (P + CP - 1) / CP;
   const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
   c->pdl = pdl_enabled() && nchunks == 1;
+  const size_t cw = (size_t)ps.W * c->compact_elems();  // one slot set: W compact states
   TRY(c->inter.alloc(per_phase * CP * lanes));
-  TRY(c->slots.alloc((size_t)lanes * Gc * c->compact_elems()));
+  TRY(c->slots.alloc((size_t)lanes * Gc * cw));
   static const bool poison = getenv("PSWE_DEBUG_POISON") != nullptr;
   if (poison) {  // debug: NaN-fill every scratch and the output, exposing entries read before written
     CU(cudaMemsetAsync(c->inter.p, 0xFF, per_phase * CP * lanes * sizeof(double2), st));
-    CU(cudaMemsetAsync(c->slots.p, 0xFF, (size_t)lanes * Gc * c->compact_elems() * sizeof(double2), st));
-    CU(cudaMemsetAsync(Ac, 0xFF, c->compact_elems() * sizeof(double2), st));
+    if (!ps.win) CU(cudaMemsetAsync(c->slots.p, 0xFF, (size_t)lanes * Gc * cw * sizeof(double2), st));
+    CU(cudaMemsetAsync(Ac, 0xFF, cw * sizeof(double2), st));
   }
-  PhaseDev ph{s, w, P};
+  // window batch: pass C adds every window segment of its phase group into
+  // zeroed slots (a group may hold several windows, a window several groups)
+  if (ps.win) CU(cudaMemsetAsync(c->slots.p, 0, (size_t)lanes * Gc * cw * sizeof(double2), st));
+  PhaseDev ph{s, ps.w, P};
+  ph.win = ps.win;
+  ph.W = ps.W;
+  ph.ustride = c->compact_elems();
   cudaStream_t lst[pswe_ctx::MAX_LANES] = {st, c->st_lane[0], c->st_lane[1], c->st_lane[2]};
   CUtensorMap mrow[pswe_ctx::MAX_LANES], mcol[pswe_ctx::MAX_LANES];
   for (int L = 0; L < lanes; ++L) {
@@ -557,7 +616,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     CU(cudaEventRecord(c->ev_fork, st));
     for (int L = 1; L < lanes; ++L) CU(cudaStreamWaitEvent(lst[L], c->ev_fork, 0));
   }
-  const bool direct = nchunks == 1 && Gc == 1;
+  const bool direct = nchunks == 1 && Gc == 1 && !ps.win;
   int chunk = 0;
   for (int p0 = 0; p0 < P; p0 += CP, ++chunk) {
     const int np = std::min(CP, P - p0);
@@ -566,7 +625,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     double2* I2 = I1 + (size_t)5 * c->Ky * c->nx * CP;
     // a single slot (one chunk, Gc = 1, e.g. the fine-step reference's one
     // node) is the output itself: pass C writes it, no reduction launch
-    double2* sl = direct ? Ac : c->slots.p + (size_t)L * Gc * c->compact_elems();
+    double2* sl = direct ? Ac : c->slots.p + (size_t)L * Gc * cw;
     TRY(dispatchA(c, ph, p0, np, Uc, I1, gate_bit >= 0 ? c->hgate.p + 4 : nullptr, lst[L]));
     TRY(dispatchB(c, np, lanes, mrow[L], mcol[L], I2, lst[L]));
     TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
@@ -576,7 +635,7 @@ int rhs_compact(pswe_ctx* c, const double* s, const double* w, int P, const doub
     CU(cudaStreamWaitEvent(st, c->ev_lane[L - 1], 0));
   }
   if (!direct) {
-    const size_t n = c->compact_elems();
+    const size_t n = cw;
     ProfScope ps(c, 3, st);
     CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, n), 256, 0, st, (const double2*)c->slots.p, lanes * Gc, n,
                 Ac));
@@ -711,49 +770,58 @@ Full3 f3c(const Full3w& a) { return Full3{a.u, a.v, a.e}; }
 // HERM_BIT_RHS = the gate flagged a standalone evaluation's input
 constexpr int HERM_BIT0 = 9, HERM_BIT_RHS = 12;
 
-int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
-  const size_t n = c->full_elems();
-  TRY(ensure_compact(c));
-  TRY(c->full_tmp.alloc(n * 18));
-  Full3w edt{c->full_tmp.p, c->full_tmp.p + n, c->full_tmp.p + 2 * n};
-  Full3w u1{c->full_tmp.p + 3 * n, c->full_tmp.p + 4 * n, c->full_tmp.p + 5 * n};
-  Full3w u2{c->full_tmp.p + 6 * n, c->full_tmp.p + 7 * n, c->full_tmp.p + 8 * n};
+// One transformed SSPRK3 step of W windows (W = 1: the ordinary step) from
+// U to out.  `tmp` holds the stage states edt, u1, u2 (3 x W states of 3n,
+// window w's at + w * 3n); U / out may be separate field pointers when
+// W = 1, else [W][3][n] blocks with window stride ws = 3n.  Uc / Ac: W
+// compact states.
+int step_impl_w(pswe_ctx* c, const PhaseSet& ps, double dt, Full3 U, Full3w out, double2* tmp, double2* Uc,
+                double2* Ac, cudaStream_t st) {
+  const size_t n = c->full_elems(), ws = 3 * n;
+  const int W = ps.W;
+  Full3w edt{tmp, tmp + n, tmp + 2 * n};
+  Full3w u1{tmp + 3 * W * n, tmp + 3 * W * n + n, tmp + 3 * W * n + 2 * n};
+  Full3w u2{tmp + 6 * W * n, tmp + 6 * W * n + n, tmp + 6 * W * n + 2 * n};
   const GridDev G = c->grid();
   const Prop pr = c->prop();
-  const int P = (int)c->s_live.size();
-  TRY(ensure_hgate(c, P));
-  const int gb = elem_grid(c, n);
+  TRY(ensure_hgate(c, ps.P));
+  const int gb = elem_grid(c, (size_t)W * n), gp = elem_grid(c, (size_t)W * c->compact_elems());
   // stage 1
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, U.u, U.v, U.e, c->Uc.p,
-              c->hgate.p));
+  CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, U.u, U.v, U.e, Uc, c->hgate.p, W, ws));
   c->launches++;
-  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st, HERM_BIT0));
+  TRY(rhs_compact(c, ps, Uc, Ac, st, HERM_BIT0));
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)c->Ac.p, edt, u1, c->flags.p));
+  CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)Ac, edt, u1, c->flags.p, W, ws));
   c->launches++;
   // stage 2
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, (const double2*)u1.u,
-              (const double2*)u1.v, (const double2*)u1.e, c->Uc.p, c->hgate.p));
+  CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, (const double2*)u1.u, (const double2*)u1.v,
+              (const double2*)u1.e, Uc, c->hgate.p, W, ws));
   c->launches++;
-  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st, HERM_BIT0 + 1));
+  TRY(rhs_compact(c, ps, Uc, Ac, st, HERM_BIT0 + 1));
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, stage2_kernel, gb, 256, 0, st, G, pr, dt, U, f3c(u1), (const double2*)c->Ac.p, u2,
-              c->flags.p));
+  CU(launch_k(c->pdl, stage2_kernel, gb, 256, 0, st, G, pr, dt, U, f3c(u1), (const double2*)Ac, u2, c->flags.p, W,
+              ws));
   c->launches++;
   // stage 3
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, elem_grid(c, c->compact_elems()), 256, 0, st, G, (const double2*)u2.u,
-              (const double2*)u2.v, (const double2*)u2.e, c->Uc.p, c->hgate.p));
+  CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, (const double2*)u2.u, (const double2*)u2.v,
+              (const double2*)u2.e, Uc, c->hgate.p, W, ws));
   c->launches++;
-  TRY(rhs_compact(c, c->s_dev.p, c->w_dev.p, P, c->Uc.p, c->Ac.p, st, HERM_BIT0 + 2));
+  TRY(rhs_compact(c, ps, Uc, Ac, st, HERM_BIT0 + 2));
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, stage3_kernel, gb, 256, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)c->Ac.p, out,
-              c->flags.p));
+  CU(launch_k(c->pdl, stage3_kernel, gb, 256, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)Ac, out,
+              c->flags.p, W, ws));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
+}
+
+int step_impl(pswe_ctx* c, double dt, Full3 U, Full3w out, cudaStream_t st) {
+  TRY(ensure_compact(c));
+  TRY(c->full_tmp.alloc(c->full_elems() * 18));
+  return step_impl_w(c, quad_phases(c), dt, U, out, c->full_tmp.p, c->Uc.p, c->Ac.p, st);
 }
 
 int decode_flags(int bits, int* stage, int* field) {
@@ -803,7 +871,9 @@ int step_verdict(pswe_ctx* c, int bits, Full3 in, cudaStream_t st, int* stage, i
 // configuration version).  Every buffer it touches is allocated by the
 // un-captured first step, so nothing allocates during capture.
 int ensure_step_graph(pswe_ctx* c, double dt, Full3 Ain, Full3w Bout, size_t bytes3, cudaStream_t st) {
-  if (c->step_exec && c->graph_dt == dt && c->graph_version == c->version && c->graph_A == Ain.u) return PSWE_OK;
+  if (c->step_exec && c->graph_dt == dt && c->graph_version == c->version && c->graph_A == Ain.u &&
+      c->graph_gen == g_alloc_gen)
+    return PSWE_OK;
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   c->step_exec = nullptr;
   const bool prof = c->prof;
@@ -837,6 +907,7 @@ int ensure_step_graph(pswe_ctx* c, double dt, Full3 Ain, Full3w Bout, size_t byt
   c->graph_dt = dt;
   c->graph_version = c->version;
   c->graph_A = Ain.u;
+  c->graph_gen = g_alloc_gen;
   return PSWE_OK;
 }
 
@@ -957,8 +1028,11 @@ void pswe_destroy(pswe_ctx* c) {
   for (DevBuf<double>* b : {&c->kxc, &c->kyc, &c->kxf, &c->kyf, &c->s_dev, &c->w_dev, &c->zero_s, &c->one_w, &c->a_dev})
     b->release();
   for (DevBuf<double2>* b : {&c->twx, &c->twy, &c->bc, &c->inter, &c->slots, &c->Uc, &c->Ac, &c->Ac2, &c->full_tmp,
-                             &c->bfull, &c->diag_cols})
+                             &c->bfull, &c->diag_cols, &c->ctab_q, &c->ctab_0, &c->ctab_b, &c->b_full, &c->b_Uc,
+                             &c->b_Ac})
     b->release();
+  for (DevBuf<double>* b : {&c->bs_dev, &c->bw_dev, &c->hgate, &c->hout}) b->release();
+  c->bwin_dev.release();
   c->diag_part.release();
   c->flags.release();
   if (c->flags_host) cudaFreeHost(c->flags_host);
@@ -970,6 +1044,7 @@ void pswe_destroy(pswe_ctx* c) {
     if (c->st_lane[L]) cudaStreamDestroy(c->st_lane[L]);
   }
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  if (c->bstep_exec) cudaGraphExecDestroy(c->bstep_exec);
   if (c->ev_run) cudaEventDestroy(c->ev_run);
   if (c->st_run) cudaStreamDestroy(c->st_run);
   delete c;
@@ -987,7 +1062,7 @@ int pswe_set_topography(pswe_ctx* c, const double* b_dev, void* stream) {
   TRY(ensure_hgate(c, 1));
   double* bstat = c->hgate.p + 1;  // scratch slots 1..3 (the statistic of field 0 lands in slot 1)
   CU(cudaMemsetAsync(bstat, 0, 3 * sizeof(double), st));
-  pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p, bstat);
+  pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, st>>>(G, b, b, b, c->Uc.p, bstat, 1, (size_t)0);
   c->launches++;
   CU(cudaMemcpyAsync(c->bc.p, c->Uc.p, (size_t)c->Ky * c->Kx * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   TRY(c->bfull.alloc(c->full_elems()));
@@ -1072,7 +1147,7 @@ int pswe_pack(pswe_ctx* c, const double* u, const double* v, const double* e, do
   if (!c || !u || !v || !e || !Uc) return set_err(PSWE_EINVAL, "null argument");
   CU(cudaSetDevice(c->device));
   pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, (cudaStream_t)stream>>>(
-      c->grid(), (const double2*)u, (const double2*)v, (const double2*)e, (double2*)Uc, nullptr);
+      c->grid(), (const double2*)u, (const double2*)v, (const double2*)e, (double2*)Uc, nullptr, 1, (size_t)0);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -1082,7 +1157,7 @@ int pswe_unpack(pswe_ctx* c, const double* Uc, double* u, double* v, double* e, 
   if (!c || !u || !v || !e || !Uc) return set_err(PSWE_EINVAL, "null argument");
   CU(cudaSetDevice(c->device));
   unpack_kernel<<<elem_grid(c, c->full_elems()), 256, 0, (cudaStream_t)stream>>>(
-      c->grid(), (const double2*)Uc, (double2*)u, (double2*)v, (double2*)e);
+      c->grid(), (const double2*)Uc, (double2*)u, (double2*)v, (double2*)e, 1, (size_t)0);
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -1093,7 +1168,7 @@ int pswe_averaged_tendency_compact(pswe_ctx* c, const double* Uc, double* Ac, vo
   if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
   TRY(check_nodes(c));
   CU(cudaSetDevice(c->device));
-  return rhs_compact(c, c->s_dev.p, c->w_dev.p, (int)c->s_live.size(), (const double2*)Uc, (double2*)Ac,
+  return rhs_compact(c, quad_phases(c), (const double2*)Uc, (double2*)Ac,
                      (cudaStream_t)stream);
 }
 
@@ -1101,22 +1176,22 @@ int pswe_averaged_tendency_compact(pswe_ctx* c, const double* Uc, double* Ac, vo
 // nodes (s_dev, P) with the gate's verdict, unpack, synchronise, and the
 // exact check when flagged (node-wrapped message when `k` is given)
 static int gated_rhs(pswe_ctx* c, const double* u, const double* v, const double* e, double* du, double* dv,
-                     double* de, const double* s_dev, const double* w_dev, const std::vector<double>& s_host,
-                     const std::vector<int>* k, cudaStream_t st) {
+                     double* de, const PhaseSet& ps, const std::vector<double>& s_host, const std::vector<int>* k,
+                     cudaStream_t st) {
   CU(cudaSetDevice(c->device));
   TRY(ensure_compact(c));
-  const int P = (int)s_host.size();
-  TRY(ensure_hgate(c, P));
+  TRY(ensure_hgate(c, ps.P));
   CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
   pack_kernel<<<elem_grid(c, c->compact_elems()), 256, 0, st>>>(c->grid(), (const double2*)u, (const double2*)v,
-                                                               (const double2*)e, c->Uc.p, c->hgate.p);
+                                                               (const double2*)e, c->Uc.p, c->hgate.p, 1,
+                                                               (size_t)0);
   c->launches++;
   CU(cudaGetLastError());
-  TRY(rhs_compact(c, s_dev, w_dev, P, c->Uc.p, c->Ac.p, st, HERM_BIT_RHS));
+  TRY(rhs_compact(c, ps, c->Uc.p, c->Ac.p, st, HERM_BIT_RHS));
   TRY(pswe_unpack(c, (const double*)c->Ac.p, du, dv, de, st));
   CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  if (*c->flags_host & (1 << HERM_BIT_RHS)) return exact_gate(c, s_dev, s_host, k, f3(u, v, e), st);
+  if (*c->flags_host & (1 << HERM_BIT_RHS)) return exact_gate(c, ps.s, s_host, k, f3(u, v, e), st);
   return PSWE_OK;
 }
 
@@ -1125,13 +1200,13 @@ int pswe_averaged_tendency(pswe_ctx* c, const double* u, const double* v, const 
   if (!c || !u || !v || !e || !du || !dv || !de) return set_err(PSWE_EINVAL, "null argument");
   if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
   TRY(check_nodes(c));
-  return gated_rhs(c, u, v, e, du, dv, de, c->s_dev.p, c->w_dev.p, c->s_live, &c->k_live, (cudaStream_t)stream);
+  return gated_rhs(c, u, v, e, du, dv, de, quad_phases(c), c->s_live, &c->k_live, (cudaStream_t)stream);
 }
 
 int pswe_apply_nonlinear(pswe_ctx* c, const double* u, const double* v, const double* e, double* du, double* dv,
                          double* de, void* stream) {
   if (!c || !u || !v || !e || !du || !dv || !de) return set_err(PSWE_EINVAL, "null argument");
-  return gated_rhs(c, u, v, e, du, dv, de, c->zero_s.p, c->one_w.p, c->zero_live, nullptr, (cudaStream_t)stream);
+  return gated_rhs(c, u, v, e, du, dv, de, zero_phases(c), c->zero_live, nullptr, (cudaStream_t)stream);
 }
 
 int pswe_apply_linear(pswe_ctx* c, const double* u, const double* v, const double* e, double* lu, double* lv,
@@ -1281,6 +1356,178 @@ done:
   CU(cudaMemcpyAsync(u, A, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(v, A + n, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(e, A + 2 * n, n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  CU(cudaEventRecord(c->ev_run, st));
+  CU(cudaStreamWaitEvent(ust, c->ev_run, 0));
+  return rc;
+}
+
+// ---------------------------------------------------------------- window batch
+int pswe_set_window_batch(pswe_ctx* c, int W, const int* n_nodes, const double* s, const double* w) {
+  if (!c || !n_nodes || !s || !w) return set_err(PSWE_EINVAL, "null argument");
+  if (W < 1) return set_err(PSWE_EINVAL, "need at least one window, got %d", W);
+  CU(cudaSetDevice(c->device));
+  std::vector<double> bs, bw;
+  std::vector<int> bwin, bk;
+  size_t off = 0;
+  for (int i = 0; i < W; ++i) {
+    const int n = n_nodes[i];
+    if (n < 1 || n % 2 != 1) return set_err(PSWE_EINVAL, "window %d: need an odd number of nodes (2M+1), got %d", i, n);
+    const int M = (n - 1) / 2;
+    int live = 0;
+    for (int k = 0; k < n; ++k)
+      if (w[off + k] != 0.0) {
+        bs.push_back(s[off + k]);
+        bw.push_back(w[off + k]);
+        bwin.push_back(i);
+        bk.push_back(k - M);
+        ++live;
+      }
+    if (!live) return set_err(PSWE_EINVAL, "window %d: quadrature has no node with nonzero weight", i);
+    off += n;
+  }
+  if (c->bW == W && bs == c->b_s && bw == c->b_w && bwin == c->b_win) return PSWE_OK;
+  const size_t P = bs.size();
+  TRY(c->bs_dev.alloc(P));
+  TRY(c->bw_dev.alloc(P));
+  TRY(c->bwin_dev.alloc(P));
+  CU(cudaMemcpy(c->bs_dev.p, bs.data(), P * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(c->bw_dev.p, bw.data(), P * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(c->bwin_dev.p, bwin.data(), P * sizeof(int), cudaMemcpyHostToDevice));
+  c->bW = W;
+  c->b_s = bs;
+  c->b_w = bw;
+  c->b_win = bwin;
+  c->b_k = bk;
+  c->ctab_b_valid = false;
+  c->version++;
+  return PSWE_OK;
+}
+
+static int check_batch_nodes(const pswe_ctx* c) {
+  std::string msg;
+  for (size_t i = 0; i < c->b_s.size(); ++i)
+    if (check_cheb(c, c->b_s[i], &msg) != PSWE_OK)
+      return set_err(PSWE_EINVAL, "window %d: averaging node k = %d (s = %.6g s) failed: %s", c->b_win[i],
+                     c->b_k[i], c->b_s[i], msg.c_str());
+  return PSWE_OK;
+}
+
+int pswe_window_batch_tendency(pswe_ctx* c, const double* Uc, double* Ac, void* stream) {
+  if (!c || !Uc || !Ac) return set_err(PSWE_EINVAL, "null argument");
+  if (c->bW < 1) return set_err(PSWE_ESTATE, "no window batch set (pswe_set_window_batch)");
+  TRY(check_batch_nodes(c));
+  CU(cudaSetDevice(c->device));
+  return rhs_compact(c, batch_phases(c), (const double2*)Uc, (double2*)Ac, (cudaStream_t)stream);
+}
+
+// capture "batched step A -> B, copy B -> A" (cached per dt / configuration)
+static int ensure_batch_graph(pswe_ctx* c, double dt, Full3 Ain, Full3w Bout, size_t bytes, cudaStream_t st) {
+  if (c->bstep_exec && c->bgraph_dt == dt && c->bgraph_version == c->version && c->bgraph_gen == g_alloc_gen)
+    return PSWE_OK;
+  if (c->bstep_exec) cudaGraphExecDestroy(c->bstep_exec);
+  c->bstep_exec = nullptr;
+  const bool prof = c->prof;
+  c->prof = false;
+  const int64_t l0 = c->launches;
+  int64_t v0[PSWE_NUM_VARIANTS];
+  std::copy(c->variant, c->variant + PSWE_NUM_VARIANTS, v0);
+  CU(cudaStreamSynchronize(st));
+  std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
+  CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+  int rc = step_impl_w(c, batch_phases(c), dt, Ain, Bout, c->b_full.p, c->b_Uc.p, c->b_Ac.p, st);
+  cudaError_t ce = cudaMemcpyAsync((void*)Ain.u, Bout.u, bytes, cudaMemcpyDeviceToDevice, st);
+  cudaGraph_t g = nullptr;
+  cudaError_t ee = cudaStreamEndCapture(st, &g);
+  c->prof = prof;
+  if (rc != PSWE_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  CU(ce);
+  CU(ee);
+  cudaError_t ie = cudaGraphInstantiate(&c->bstep_exec, g, 0);
+  cudaGraphDestroy(g);
+  CU(ie);
+  c->bstep_graph_launches = c->launches - l0;
+  c->launches = l0;
+  for (int i = 0; i < PSWE_NUM_VARIANTS; ++i) {
+    c->bgraph_variant[i] = c->variant[i] - v0[i];
+    c->variant[i] = v0[i];
+  }
+  c->bgraph_dt = dt;
+  c->bgraph_version = c->version;
+  c->bgraph_gen = g_alloc_gen;
+  return PSWE_OK;
+}
+
+int pswe_window_batch_run(pswe_ctx* c, double dt, int nsteps, double* U, int* bad_step, void* stream) {
+  if (!c || !U) return set_err(PSWE_EINVAL, "null argument");
+  if (bad_step) *bad_step = 0;
+  if (nsteps < 0) return set_err(PSWE_EINVAL, "nsteps must be nonnegative, got %d", nsteps);
+  if (nsteps == 0) return PSWE_OK;
+  if (c->bW < 1) return set_err(PSWE_ESTATE, "no window batch set (pswe_set_window_batch)");
+  if (!(dt > 0)) return set_err(PSWE_EINVAL, "dt must be positive, got %g", dt);
+  std::string msg;
+  if (check_cheb(c, dt, &msg) != PSWE_OK) return set_err(PSWE_EINVAL, "%s", msg.c_str());
+  TRY(check_batch_nodes(c));
+  CU(cudaSetDevice(c->device));
+  cudaStream_t ust = (cudaStream_t)stream;
+  cudaStream_t st = c->st_run;
+  CU(cudaEventRecord(c->ev_run, ust));
+  CU(cudaStreamWaitEvent(st, c->ev_run, 0));
+  const int W = c->bW;
+  const size_t n = c->full_elems(), sw = (size_t)3 * W * n;  // one batch state: W x 3 fields
+  TRY(c->b_full.alloc(6 * sw));
+  TRY(c->b_Uc.alloc((size_t)W * c->compact_elems()));
+  TRY(c->b_Ac.alloc((size_t)W * c->compact_elems()));
+  double2* A = c->b_full.p + 3 * sw;
+  double2* B = c->b_full.p + 4 * sw;
+  double2* S = c->b_full.p + 5 * sw;
+  const size_t bytes = sw * sizeof(double2);
+  CU(cudaMemcpyAsync(A, U, bytes, cudaMemcpyDeviceToDevice, st));
+  const Full3 Ain{A, A + n, A + 2 * n};
+  const Full3w Bout{B, B + n, B + 2 * n};
+  int rc = PSWE_OK;
+  // any flag (a non-finite stage or the Hermitian gate) stops the batch at
+  // the start of the flagged step; the caller re-runs the windows one by
+  // one for the reference's per-window error
+  auto flagged = [&](int i) {
+    if (bad_step) *bad_step = i;
+    rc = set_err(PSWE_ENONFINITE, "window batch flagged at step %d", i);
+  };
+  int i = 1;
+  CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
+  TRY(step_impl_w(c, batch_phases(c), dt, Ain, Bout, c->b_full.p, c->b_Uc.p, c->b_Ac.p, st));
+  CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (*c->flags_host) {
+    flagged(1);
+    goto done;
+  }
+  CU(cudaMemcpyAsync(A, B, bytes, cudaMemcpyDeviceToDevice, st));
+  ++i;
+  if (i <= nsteps) {
+    TRY(ensure_batch_graph(c, dt, Ain, Bout, bytes, st));
+    const int batch = 16;
+    while (i <= nsteps) {
+      const int k = std::min(batch, nsteps - i + 1);
+      CU(cudaMemcpyAsync(S, A, bytes, cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
+      for (int j = 0; j < k; ++j) CU(cudaGraphLaunch(c->bstep_exec, st));
+      c->launches += (int64_t)k * c->bstep_graph_launches;
+      for (int v = 0; v < PSWE_NUM_VARIANTS; ++v) c->variant[v] += (int64_t)k * c->bgraph_variant[v];
+      CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      if (*c->flags_host) {
+        CU(cudaMemcpyAsync(A, S, bytes, cudaMemcpyDeviceToDevice, st));
+        flagged(i);
+        goto done;
+      }
+      i += k;
+    }
+  }
+done:
+  CU(cudaMemcpyAsync(U, A, bytes, cudaMemcpyDeviceToDevice, st));
   CU(cudaEventRecord(c->ev_run, st));
   CU(cudaStreamWaitEvent(ust, c->ev_run, 0));
   return rc;

@@ -56,6 +56,13 @@ struct PhaseDev {
   const double* s;  // [P] live node shifts, ascending k
   const double* w;  // [P] weights
   int P;
+  // window batch (window sweep): the phases of W
+  // windows concatenated, win[p] = window of phase p; window w's compact
+  // state is Uc + w * ustride and its slots follow the previous window's.
+  // win == nullptr: one window.
+  const int* win = nullptr;
+  int W = 1;
+  size_t ustride = 0;
 };
 
 // compact kx index of FFT position k (0..nx-1), or -1 outside the band
@@ -119,17 +126,20 @@ __device__ __forceinline__ void store_t1_strided(const double2* v, int t, double
   }
 }
 
-template <int NX>
+template <int NX, bool MW = false>
 struct PassAW {
   static constexpr int T = WF<NX>::T, P = WF<NX>::P, GPW = WF<NX>::GPW;
   static constexpr int WARPS = 5;
   // 3 CTAs/SM (no spills for nx >= 32); at 4 CTAs/SM (96 registers) the
   // phase-pair block spills and measured slower
   static constexpr int CTAS = 3;
-  // mbarrier | buffer [6][GPW][Kx] (u, v, eta, b, (c1,c2)_p, (c1,c2)_q ->
-  // u'_p, v'_p, depth_p, u'_q, v'_q, depth_q in place) | xbuf per group
+  // mbarrier | buffer [SLOTS][GPW][Kx] (u, v, eta, b, (c1,c2)_p, (c1,c2)_q ->
+  // u'_p, v'_p, depth_p, u'_q, v'_q, depth_q in place; window batches (MW)
+  // add u, v, eta of phase q's window in slots 6..8 when it differs from p's)
+  // | xbuf per group
+  static constexpr int SLOTS = MW ? 9 : 6;
   static size_t bytes(int Kx) {
-    return 16 + (size_t)GPW * 6 * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
+    return 16 + (size_t)GPW * SLOTS * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
   }
 };
 
@@ -141,20 +151,20 @@ struct PassAW {
 // for both phases), then warp f runs the inverse x-FFTs of output field f
 // (u, v, eta-b, ikx u, ikx v) of both phases and stores them to I1.  Two CTA
 // barriers per two transforms per warp.
-template <int NX>
-__global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
+template <int NX, bool MW>
+__global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CTAS)
     passA_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, const double2* __restrict__ Uc,
                  const double2* __restrict__ ctab, double2* __restrict__ I, double* __restrict__ pscale) {
   griddep_wait();
   griddep_launch();
-  using W = PassAW<NX>;
+  using W = PassAW<NX, MW>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW;
   extern __shared__ __align__(128) unsigned char sbytes[];
   constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
   const int Ky = G.Ky;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
-  double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [6][GPW][Kx]
-  double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * 6 * Kx);
+  double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [SLOTS][GPW][Kx]
+  double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * W::SLOTS * Kx);
   const bool tab = ctab != nullptr;
   const int cols = (Ky + GPW - 1) / GPW;
   const int npair = (np + 1) / 2;
@@ -164,17 +174,30 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
 
   // block -> (phase pair pp, first column j0, ncol columns): contiguous in U, b, ctab.
   // Warp 0: lane 0 posts the byte count, lanes 0..5 each issue one bulk copy.
+  // window batch: the windows of the block's two phases (MW only)
+  auto wins = [&](int pp, int& wp, int& wq) {
+    wp = wq = 0;
+    if constexpr (MW) {
+      wp = ph.win[p0 + 2 * pp];
+      wq = (2 * pp + 1 < np) ? ph.win[p0 + 2 * pp + 1] : wp;
+    }
+  };
   auto prefetch = [&](int blk) {
     const int pp = blk / cols, j0 = (blk % cols) * GPW;
     const int ncol = min(GPW, Ky - j0);
     const int nq = (2 * pp + 1 < np) ? 2 : 1;
+    int wp, wq;
+    wins(pp, wp, wq);
     const uint32_t seg = (uint32_t)(ncol * Kx * sizeof(double2));
-    if (lane == 0) mbar_arrive_expect_tx(bar, (tab ? 4 + nq : 4) * seg);
+    if (lane == 0) mbar_arrive_expect_tx(bar, ((tab ? 4 + nq : 4) + (wq != wp ? 3 : 0)) * seg);
     __syncwarp();
-    if (lane < 3) bulk_g2s(buf + lane * fs, Uc + lane * KyKx + (size_t)j0 * Kx, seg, bar);
+    const double2* Up = Uc + (size_t)wp * ph.ustride;
+    if (lane < 3) bulk_g2s(buf + lane * fs, Up + lane * KyKx + (size_t)j0 * Kx, seg, bar);
     if (lane == 3) bulk_g2s(buf + 3 * fs, G.bc + (size_t)j0 * Kx, seg, bar);
     if (tab && lane >= 4 && lane - 4 < nq)
       bulk_g2s(buf + lane * fs, ctab + (size_t)(p0 + 2 * pp + lane - 4) * KyKx + (size_t)j0 * Kx, seg, bar);
+    if (MW && wq != wp && lane >= 6 && lane < 9)
+      bulk_g2s(buf + lane * fs, Uc + (size_t)wq * ph.ustride + (lane - 6) * KyKx + (size_t)j0 * Kx, seg, bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
@@ -195,6 +218,9 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
     const int ncol = min(GPW, Ky - j0);
     const int pa = 2 * pp;
     const bool hasq = pa + 1 < np;
+    int wp, wq;
+    wins(pp, wp, wq);
+    const bool qown = MW && wq != wp;  // phase q's state is in slots 6..8
     mbar_wait(bar, it & 1);
     // e^{sL} per mode for both phases, in place:
     // (u, v, eta, b, c_p, c_q) -> (u', v', eta' - b)_p, (u', v', eta' - b)_q, / (nx ny)
@@ -214,10 +240,11 @@ __global__ void __launch_bounds__(PassAW<NX>::WARPS * 32, PassAW<NX>::CTAS)
       for (int c = 1; c < GPW; ++c)
         if (tt == c) ky = kyb[c];
       const double2 cb = (tab && hasq) ? e[5 * fs] : czero();
+      const C3 q1 = qown ? C3{e[6 * fs], e[7 * fs], e[8 * fs]} : q0;
 #pragma unroll 1
       for (int sub = 0; sub < (hasq ? 2 : 1); ++sub) {
-        C3 q = tab ? exp_c12(sub ? cb : e[4 * fs], q0, G.ph, kx, ky)
-                   : expL(ph.s[p0 + pa + sub], q0, G.ph, kx, ky, pr);
+        C3 q = tab ? exp_c12(sub ? cb : e[4 * fs], sub ? q1 : q0, G.ph, kx, ky)
+                   : expL(ph.s[p0 + pa + sub], sub ? q1 : q0, G.ph, kx, ky, pr);
         double2* o = e + (size_t)(3 * sub) * fs;
         const double2 dep = csub(q.e, bb);
         o[0] = cscale(G.inv_n2, q.u);
@@ -878,7 +905,7 @@ struct PassCW {
 // overlay the consumed input); then every thread combines its modes (flux
 // divergence, e^{-sL}, weight) into register accumulators, which are added
 // to the group's slot once at the end.
-template <int NX>
+template <int NX, bool MW>
 __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
     passC_kernel(GridDev G, Prop pr, PhaseDev ph, int p0, int np, int Gc, const double2* __restrict__ I2,
                  const double2* __restrict__ ctab, double2* __restrict__ slots, int first_chunk) {
@@ -936,8 +963,37 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   C3 acc[CPT];
 #pragma unroll
   for (int c = 0; c < CPT; ++c) acc[c] = c3zero();
+  // slot (+)= acc: this group's phases (of one window), in chunk order.  A
+  // window batch (MW) zero-fills the slots first and flushes at every window
+  // boundary into slot [g][window].
+  auto flush = [&](int win, bool add) {
+    double2* slot = slots + ((size_t)g * ph.W + win) * 3 * KyKx;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int idx = threadIdx.x + c * W::WARPS * 32;
+      const int tt = idx / Kx, r = idx % Kx;
+      if (tt < ncol) {
+        double2* sp = slot + (size_t)(j0 + tt) * Kx + r;
+        C3 a = acc[c];
+        if (add) a = c3add({sp[0], sp[KyKx], sp[2 * KyKx]}, a);
+        sp[0] = a.u;
+        sp[KyKx] = a.v;
+        sp[2 * KyKx] = a.e;
+      }
+    }
+  };
+  int wcur = MW && lo < hi ? ph.win[p0 + lo] : 0;
 #pragma unroll 1
   for (int pl = lo; pl < hi; ++pl) {
+    if constexpr (MW) {
+      const int wn = ph.win[p0 + pl];
+      if (wn != wcur) {
+        flush(wcur, true);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[c] = c3zero();
+        wcur = wn;
+      }
+    }
     const int b = (pl - lo) & 1;
     double2* pre = pre0 + b * PB;
     mbar_wait(bar + b, ((pl - lo) >> 1) & 1);
@@ -980,20 +1036,10 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
     __syncthreads();  // buffer b consumed
     if (f == 0 && pl + 2 < hi) prefetch(pl + 2);
   }
-  // slot (+)= this group's phases, in chunk order
-  double2* slot = slots + (size_t)g * 3 * KyKx;
-#pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int idx = threadIdx.x + c * W::WARPS * 32;
-    const int tt = idx / Kx, r = idx % Kx;
-    if (tt < ncol) {
-      double2* sp = slot + (size_t)(j0 + tt) * Kx + r;
-      C3 a = acc[c];
-      if (!first_chunk) a = c3add({sp[0], sp[KyKx], sp[2 * KyKx]}, a);
-      sp[0] = a.u;
-      sp[KyKx] = a.v;
-      sp[2 * KyKx] = a.e;
-    }
+  if (MW) {
+    if (lo < hi) flush(wcur, true);
+  } else {
+    flush(0, !first_chunk);
   }
 }
 
@@ -1017,22 +1063,26 @@ __global__ void reduce_slots_kernel(const double2* __restrict__ slots, int Gc, s
 // also the Hermitian gate's statistic: hstat[f] = max over the band of
 // |c(k) - conj c(-k)|^2 per field (herm_kernels.cuh; NaN propagates).
 __global__ void pack_kernel(GridDev G, const double2* __restrict__ u, const double2* __restrict__ v,
-                            const double2* __restrict__ e, double2* __restrict__ Uc, double* __restrict__ hstat) {
+                            const double2* __restrict__ e, double2* __restrict__ Uc, double* __restrict__ hstat,
+                            int W, size_t ws) {
   griddep_wait();
   griddep_launch();
+  // W windows (a window batch): window w's fields at + w * ws, its compact state at + w * 3 Ky Kx
   const size_t KyKx = (size_t)G.Ky * G.Kx;
   double dmax[3] = {0.0, 0.0, 0.0};
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 3 * KyKx; i += (size_t)gridDim.x * blockDim.x) {
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < (size_t)W * 3 * KyKx;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t win = t / (3 * KyKx), i = t - win * 3 * KyKx;
     const int f = (int)(i / KyKx);
     const int rem = (int)(i % KyKx);
     const int j = rem / G.Kx, r = rem % G.Kx;
     const int wx = r <= G.kxm ? r : r - G.Kx;
     const int ix = (wx + G.nx) % G.nx, jx = (G.nx - ix) % G.nx;
     const int jy = j, my = (G.ny - j) % G.ny;
-    const double2* c = f == 0 ? u : (f == 1 ? v : e);
+    const double2* c = (f == 0 ? u : (f == 1 ? v : e)) + win * ws;
     const double2 a = c[(size_t)ix * G.ny + jy];
     const double2 b = c[(size_t)jx * G.ny + my];
-    Uc[i] = cmk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+    Uc[t] = cmk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
     if (hstat) {
       const double dx = a.x - b.x, dy = a.y + b.y;
       const double d2 = fma(dx, dx, dy * dy);
@@ -1071,16 +1121,19 @@ __device__ __forceinline__ C3 compact_at(const GridDev& G, const double2* __rest
 }
 
 __global__ void unpack_kernel(GridDev G, const double2* __restrict__ Ac, double2* __restrict__ u,
-                              double2* __restrict__ v, double2* __restrict__ e) {
+                              double2* __restrict__ v, double2* __restrict__ e, int W, size_t ws) {
   griddep_wait();
   griddep_launch();
-  const size_t n = (size_t)G.nx * G.ny;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+  const size_t n = (size_t)G.nx * G.ny, cs = 3 * (size_t)G.Ky * G.Kx;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < (size_t)W * n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t win = t / n, i = t - win * n;
     const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
-    C3 q = compact_at(G, Ac, ix, jy);
-    u[i] = q.u;
-    v[i] = q.v;
-    e[i] = q.e;
+    C3 q = compact_at(G, Ac + win * cs, ix, jy);
+    const size_t o = win * ws + i;
+    u[o] = q.u;
+    v[o] = q.v;
+    e[o] = q.e;
   }
 }
 
@@ -1130,23 +1183,29 @@ __device__ __forceinline__ void flag_nonfinite(const C3& q, int stage, int* flag
   if (bits && (threadIdx.x & 31) == 0) atomicOr(flags, bits);
 }
 
+// The stage kernels run over W windows (a window batch) at once: window w's
+// full-layout states at + w * ws, its compact tendency at + w * 3 Ky Kx.
+__device__ __forceinline__ Full3 wshift(const Full3& a, size_t o) { return {a.u + o, a.v + o, a.e + o}; }
+__device__ __forceinline__ Full3w wshift(const Full3w& a, size_t o) { return {a.u + o, a.v + o, a.e + o}; }
+
 // stage 1 (integrator.py:96-98): e_dt = E(dt) U;  u1 = e_dt + dt * E(dt) A(U)
 __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const double2* __restrict__ Ac,
-                              Full3w edt, Full3w u1, int* flags) {
+                              Full3w edt, Full3w u1, int* flags, int W, size_t ws) {
   griddep_wait();
   griddep_launch();
-  const size_t n = (size_t)G.nx * G.ny;
-  for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < n; i0 += (size_t)gridDim.x * blockDim.x) {
-    const size_t i = i0 + threadIdx.x;
+  const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
+  for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = i0 + threadIdx.x;
     C3 o = c3zero();
-    if (i < n) {
+    if (t < N) {
+      const size_t win = t / n, i = t - win * n;
       const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
       const double kx = G.kxf[ix], ky = G.kyf[jy];
-      const C3 e = expL(dt, ld3(U, i), G.ph, kx, ky, pr);
-      const C3 ea = expL(dt, compact_at(G, Ac, ix, jy), G.ph, kx, ky, pr);
+      const C3 e = expL(dt, ld3(wshift(U, win * ws), i), G.ph, kx, ky, pr);
+      const C3 ea = expL(dt, compact_at(G, Ac + win * cs, ix, jy), G.ph, kx, ky, pr);
       o = c3add(e, c3scale(dt, ea));
-      st3(edt, i, e);
-      st3(u1, i, o);
+      st3(wshift(edt, win * ws), i, e);
+      st3(wshift(u1, win * ws), i, o);
     }
     flag_nonfinite(o, 1, flags);
   }
@@ -1154,22 +1213,23 @@ __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const doub
 
 // stage 2 (integrator.py:99-100): u2 = 3/4 E(dt/2) U + 1/4 E(-dt/2) (u1 + dt A(u1))
 __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, const double2* __restrict__ Ac,
-                              Full3w u2, int* flags) {
+                              Full3w u2, int* flags, int W, size_t ws) {
   griddep_wait();
   griddep_launch();
-  const size_t n = (size_t)G.nx * G.ny;
+  const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   const double h = 0.5 * dt;
-  for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < n; i0 += (size_t)gridDim.x * blockDim.x) {
-    const size_t i = i0 + threadIdx.x;
+  for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = i0 + threadIdx.x;
     C3 o = c3zero();
-    if (i < n) {
+    if (t < N) {
+      const size_t win = t / n, i = t - win * n;
       const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
       const double kx = G.kxf[ix], ky = G.kyf[jy];
-      const C3 a = expL(h, ld3(U, i), G.ph, kx, ky, pr);
-      const C3 y = c3add(ld3(u1, i), c3scale(dt, compact_at(G, Ac, ix, jy)));
+      const C3 a = expL(h, ld3(wshift(U, win * ws), i), G.ph, kx, ky, pr);
+      const C3 y = c3add(ld3(wshift(u1, win * ws), i), c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
       const C3 b = expL(-h, y, G.ph, kx, ky, pr);
       o = c3add(c3scale(0.75, a), c3scale(0.25, b));
-      st3(u2, i, o);
+      st3(wshift(u2, win * ws), i, o);
     }
     flag_nonfinite(o, 2, flags);
   }
@@ -1177,21 +1237,22 @@ __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, 
 
 // stage 3 (integrator.py:101-102): out = 1/3 e_dt + 2/3 E(dt/2) (u2 + dt A(u2))
 __global__ void stage3_kernel(GridDev G, Prop pr, double dt, Full3 edt, Full3 u2, const double2* __restrict__ Ac,
-                              Full3w out, int* flags) {
+                              Full3w out, int* flags, int W, size_t ws) {
   griddep_wait();
   griddep_launch();
-  const size_t n = (size_t)G.nx * G.ny;
+  const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   const double h = 0.5 * dt;
-  for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < n; i0 += (size_t)gridDim.x * blockDim.x) {
-    const size_t i = i0 + threadIdx.x;
+  for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = i0 + threadIdx.x;
     C3 o = c3zero();
-    if (i < n) {
+    if (t < N) {
+      const size_t win = t / n, i = t - win * n;
       const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
       const double kx = G.kxf[ix], ky = G.kyf[jy];
-      const C3 y = c3add(ld3(u2, i), c3scale(dt, compact_at(G, Ac, ix, jy)));
+      const C3 y = c3add(ld3(wshift(u2, win * ws), i), c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
       const C3 b = expL(h, y, G.ph, kx, ky, pr);
-      o = c3add(c3scale(1.0 / 3.0, ld3(edt, i)), c3scale(2.0 / 3.0, b));
-      st3(out, i, o);
+      o = c3add(c3scale(1.0 / 3.0, ld3(wshift(edt, win * ws), i)), c3scale(2.0 / 3.0, b));
+      st3(wshift(out, win * ws), i, o);
     }
     flag_nonfinite(o, 3, flags);
   }

@@ -350,22 +350,70 @@ def test_graph_batched_run_matches_single_steps_bitwise():
     assert all(bool((a == b).all()) for a, b in zip(U, V))
 
 
-def test_window_sweep_matches_individual_runs_bitwise():
-    """8f item 2: all windows run concurrently (one context + stream each) and
-    each equals its own sequential run bitwise; errors vs a fine reference."""
+def test_window_sweep_batch_matches_individual_runs():
+    """8f item 2: all windows advance as one window batch (one launch
+    sequence per stage over the (window, phase) axis).  Each window equals
+    its own one-by-one run to round-off (the batch regroups the phase sums
+    and pairs phases of neighbouring windows in pass B), the batch really
+    ran (variant counts), and errors vs a fine reference are filled in."""
     c = cases.CASES["C2"]()
     dt, t_end = c.dt, 2 * c.dt
-    windows = (0.0, 1800.0, 3600.0)
+    windows = (0.0, 1800.0, 3600.0, 7200.0)
     ref = pk.run(c.state, pk.StepConfig(dt=180.0, quadrature=pk.kernel_weights(0.0, 0),
                                         propagator_spec=pk.PropagatorSpec.exact()), c.params, t_end).states[-1]
+    ctx = pk.dynamics.context(c.state, c.params)
+    before = ctx.launch_count
     res = pk.window_sweep(c.state, c.params, dt, t_end, windows, M=8, reference=ref)
+    assert ctx.launch_count > before
     assert [r.T for r in res] == list(windows)
     for r in res:
         cfg = pk.make_step_config(c.grid, c.params, dt=dt, T=r.T, M=8 if r.T > 0 else 0)
-        solo = pk.run(c.state, cfg, c.params, t_end).states[-1]
-        assert np.array_equal(arr(r.final), arr(solo))
-        assert r.final.t == solo.t
+        solo = pk.run(c.state, cfg, c.params, t_end)
+        assert rel_l2(arr(r.final), arr(solo.states[-1])) <= 1e-13
+        assert r.final.t == solo.states[-1].t
+        assert r.trajectory.steps == solo.steps
+        assert np.allclose(r.trajectory.energy, solo.energy, rtol=1e-12, atol=0)
         assert np.isfinite(r.l2_eta) and np.isfinite(r.l2_u)
+    seq = pk.window_sweep(c.state, c.params, dt, t_end, windows, M=8, batched=False)
+    for a, b in zip(res, seq):
+        assert rel_l2(arr(a.final), arr(b.final)) <= 1e-13
+
+
+def test_window_batch_matches_oracle():
+    """Two windows of different length (7 and 15 live phases) over two steps
+    with a mountain (C3's grid): each window vs the oracle's own run, and the
+    batched averaged tendencies vs the oracle per window."""
+    z = load_golden("C3")
+    grid, params, state, _ = golden_problem(z)
+    dt = float(z["dt"])
+    quads = [pk.kernel_weights(900.0, 4), pk.kernel_weights(1800.0, 8)]
+    S = O.Setup(grid.nx, grid.ny, grid.Lx, grid.Ly, params.f, params.g, params.H, params.b)
+    ctx = pk.dynamics.context(state, params)
+    ctx.set_propagator("exact")
+    ctx.set_window_batch(quads)
+    U = arr(state)
+    # tendencies: window w sees its own state (here two different states)
+    U2 = np.stack([U, 1.01 * U])
+    Uc = torch_compact(ctx, U2)
+    got = ctx.window_batch_tendency(Uc)
+    for w, q in enumerate(quads):
+        want = O.averaged_tendency(S, U2[w], q.s, q.w)
+        full = np.stack([t.cpu().numpy() for t in ctx.unpack(got[w])])
+        assert O.rel_l2(full, want) <= RHS_TOL
+    # two steps of both windows at once
+    res = pk.window_sweep(state, params, dt, 2 * dt, [900.0, 1800.0], M=None)
+    for r in res:
+        q = pk.make_step_config(grid, params, dt=dt, T=r.T).quadrature
+        want = O.run(S, U, dt, 2, q.s, q.w)
+        assert O.rel_l2(arr(r.final), want) <= STEP_TOL
+
+
+def torch_compact(ctx, U2):
+    import torch
+    out = []
+    for Uw in U2:
+        out.append(ctx.pack([ctx.to_device(x) for x in Uw]))
+    return torch.stack(out).contiguous()
 
 
 def test_chebyshev_route_step_and_run_match_oracle():
