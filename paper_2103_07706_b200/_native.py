@@ -427,6 +427,8 @@ class Context:
         if isinstance(arr, torch.Tensor):
             return arr.to(device=f"cuda:{self.device}", dtype=torch.complex128).contiguous()
         a = np.ascontiguousarray(arr, dtype=np.complex128)
+        if not a.flags.writeable:  # torch.from_numpy wants a writable buffer (it is only read here)
+            a = a.copy()
         return torch.from_numpy(a).to(device=f"cuda:{self.device}", non_blocking=False)
 
     def empty_full(self):

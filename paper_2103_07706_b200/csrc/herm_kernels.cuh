@@ -15,7 +15,8 @@
 //   pack   -> max over the band of |D_f(k)|^2, D = c(k) - conj c(-k), per field
 //   pass A -> per phase, max over the band of |e^{sL} U_h - b_h|_f^2 on the
 //             Hermitian part it propagates anyway
-//   herm_eval_kernel: e^{sL} is unitary in the energy norm
+//   herm_eval_block (by block 0 of the kernel that consumes the RHS -- the
+//             stage kernel or unpack): e^{sL} is unitary in the energy norm
 //             |x|_W^2 = H(|u|^2 + |v|^2) + g |eta|^2, so every propagated
 //             defect is at most d = |D|_W / sqrt(min(H, g)) + max|D_b| and the
 //             true scale is at least scale_h(s) - d / 2: when d < 1e-12
@@ -30,35 +31,6 @@
 #include "pswe_kernels.cuh"
 
 namespace pswe {
-
-// flags bit `bit` when some phase might fail the gate; resets the statistics
-// (hstat[3] = max |D_f|^2 of the packed input, pscale[P] = per-phase max
-// squared magnitude) for the next evaluation
-__global__ void herm_eval_kernel(double* __restrict__ hstat, double bdef, double* __restrict__ pscale, int P,
-                                 double H, double g, int* __restrict__ flags, int bit) {
-  griddep_wait();
-  griddep_launch();
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  const double dW2 = H * hstat[0] + H * hstat[1] + g * hstat[2];
-  const double d = sqrt(dW2) / sqrt(fmin(H, g)) + bdef;
-  int mine = 0;
-  if (d != 0.0) {  // an exactly Hermitian input cannot fail
-    for (int p = threadIdx.x; p < P; p += blockDim.x) {
-      const double sc = sqrt(pscale[p]);
-      // NaN anywhere makes the test false: flagged, the exact path decides
-      if (!(1.01 * d < 1e-12 * (sc - 0.5 * d))) mine = 1;
-    }
-  }
-  if (mine) bad = 1;
-  __syncthreads();  // every read precedes the resets
-  for (int p = threadIdx.x; p < P; p += blockDim.x) pscale[p] = 0.0;
-  if (threadIdx.x == 0) {
-    hstat[0] = hstat[1] = hstat[2] = 0.0;
-    if (bad) atomicOr(flags, 1 << bit);
-  }
-}
 
 // block reduction of (max, first index) pairs and nonneg maxima
 struct HermAcc {

@@ -19,6 +19,7 @@
 #include "pswe_kernels.cuh"
 #include "diag_kernels.cuh"
 #include "herm_kernels.cuh"
+#include "fused_kernels.cuh"
 
 using namespace pswe;
 
@@ -541,19 +542,60 @@ PhaseSet quad_phases(pswe_ctx* c) {
   return {c->s_dev.p, c->w_dev.p, nullptr, (int)c->s_live.size(), 1, &c->ctab_q, &c->ctab_q_valid};
 }
 PhaseSet zero_phases(pswe_ctx* c) { return {c->zero_s.p, c->one_w.p, nullptr, 1, 1, &c->ctab_0, &c->ctab_0_valid}; }
+HermGate hgate_of(pswe_ctx* c, int P, int bit) {
+  return HermGate{c->hgate.p, c->hgate.p + 4, P, c->bdef, c->H, c->g, c->flags.p, bit};
+}
+HermGate no_gate() { return HermGate{nullptr, nullptr, 0, 0.0, 1.0, 1.0, nullptr, -1}; }
+
 PhaseSet batch_phases(pswe_ctx* c) {
   return {c->bs_dev.p, c->bw_dev.p, c->bwin_dev.p, (int)c->b_s.size(), c->bW, &c->ctab_b, &c->ctab_b_valid};
 }
 
-// `gate_bit` >= 0: the input was packed with the gate's statistics
-// (pack_kernel hstat = hgate); pass A adds the per-phase scales and the
-// evaluation ends with herm_eval_kernel, which sets flags bit gate_bit when
-// the exact check has to decide.  A window batch (ps.win) evaluates W
+// Small square grids: the one-CTA-per-phase-group kernel (fused_kernels.cuh)
+template <int N, bool MW>
+int launch_fused(pswe_ctx* c, const PhaseDev& ph, int Gc, const double2* Uc, double2* out, double* pscale,
+                 cudaStream_t st) {
+  using W = FusedW<N>;
+  auto kern = fused_kernel<N, MW>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::bytes()));
+  ProfScope ps(c, 0, st);
+  CU(launch_k(c->pdl, kern, Gc, W::NT, W::bytes(), st, c->grid(), c->prop(), ph, Gc, Uc, c->ctab_cur, out, pscale));
+  c->launches++;
+  c->variant[PSWE_V_FUSED]++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+template <int N>
+int fused_capacity(const pswe_ctx* c) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<N, false>, FusedW<N>::NT,
+                                                    FusedW<N>::bytes()) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  return per_sm * c->sms;
+}
+
+// Measured (tools/fused_check.py): n <= 32 one CTA per phase group wins
+// everywhere (32^2, M = 8: 30 -> 20 us; M = 256: 131 -> 63 us); at 64^2 the
+// single CTA's 8 warps are latency-bound (M = 256: 113 -> 128 us), so 64^2
+// keeps the three-pass pipeline unless PSWE_FUSED64 is set.
+bool fused_ok(const pswe_ctx* c) {
+  static const bool off = getenv("PSWE_NO_FUSED") != nullptr;  // A/B switch
+  static const bool f64 = getenv("PSWE_FUSED64") != nullptr;
+  return !off && c->nx == c->ny && (c->nx <= 32 || (f64 && c->nx == 64));
+}
+
+// `gate`: the input was packed with the gate's statistics (pack_kernel
+// hstat = hgate) and pass A adds the per-phase scales; the kernel that
+// consumes the result evaluates them (herm_eval_block, via hgate_of) and
+// sets its flags bit when the exact check has to decide.  A window batch (ps.win) evaluates W
 // windows' tendencies at once: Uc / Ac hold W compact states.
 int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac, cudaStream_t st,
-                int gate_bit = -1) {
+                bool gate = false) {
   const double* s = ps.s;
   const int P = ps.P;
+  const bool fused = fused_ok(c);
   // exact route: phase table (built once per quadrature / grid)
   c->ctab_cur = nullptr;
   if (c->kind == 0) {
@@ -568,6 +610,49 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
     }
     c->ctab_cur = tb.p;
   }
+  if (fused) {
+    // one CTA per phase group, every resident CTA busy at most once
+    int cap = 1;
+    switch (c->nx) {
+      case 8: cap = fused_capacity<8>(c); break;
+      case 16: cap = fused_capacity<16>(c); break;
+      case 32: cap = fused_capacity<32>(c); break;
+      default: cap = fused_capacity<64>(c); break;
+    }
+    const int Gc = std::max(1, std::min(P, cap));
+    const size_t cw = (size_t)ps.W * c->compact_elems();
+    const bool direct = Gc == 1 && !ps.win;
+    c->pdl = pdl_enabled();
+    if (!direct) TRY(c->slots.alloc((size_t)Gc * cw));
+    double2* out = direct ? Ac : c->slots.p;
+    if (ps.win) CU(cudaMemsetAsync(c->slots.p, 0, (size_t)Gc * cw * sizeof(double2), st));
+    PhaseDev ph{s, ps.w, P};
+    ph.win = ps.win;
+    ph.W = ps.W;
+    ph.ustride = c->compact_elems();
+    double* pscale = gate ? c->hgate.p + 4 : nullptr;
+    int rc = PSWE_OK;
+    switch (c->nx) {
+      case 8: rc = ps.win ? launch_fused<8, true>(c, ph, Gc, Uc, out, pscale, st)
+                          : launch_fused<8, false>(c, ph, Gc, Uc, out, pscale, st); break;
+      case 16: rc = ps.win ? launch_fused<16, true>(c, ph, Gc, Uc, out, pscale, st)
+                           : launch_fused<16, false>(c, ph, Gc, Uc, out, pscale, st); break;
+      case 32: rc = ps.win ? launch_fused<32, true>(c, ph, Gc, Uc, out, pscale, st)
+                           : launch_fused<32, false>(c, ph, Gc, Uc, out, pscale, st); break;
+      default: rc = ps.win ? launch_fused<64, true>(c, ph, Gc, Uc, out, pscale, st)
+                           : launch_fused<64, false>(c, ph, Gc, Uc, out, pscale, st); break;
+    }
+    TRY(rc);
+    if (!direct) {
+      ProfScope pr3(c, 3, st);
+      CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, cw), 256, 0, st, (const double2*)c->slots.p, Gc, cw,
+                  Ac));
+      c->launches++;
+      c->variant[PSWE_V_REDUCE]++;
+      CU(cudaGetLastError());
+    }
+    return PSWE_OK;
+  }
   const size_t per_phase = (size_t)9 * c->Ky * c->nx;  // I1 (5 fields) + I2 (4 fields), double2
   // Chunk "lanes" on separate streams when there is more than one chunk:
   // the chunks' passes overlap and fill each other's launch tails.  Each lane
@@ -581,7 +666,9 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
   // at least one chunk per lane when a chunk still holds >= 16 phases and
   // >= 24 MiB of intermediates: the lanes' overlap is then worth more than
   // the larger per-launch grids of fewer chunks
-  const int minph = std::max<int>(16, (int)((size_t(24) << 20) / (per_phase * sizeof(double2))));
+  static const int minph_floor = getenv("PSWE_MINPH") ? atoi(getenv("PSWE_MINPH")) : 16;  // tuning experiments
+  static const int minmb = getenv("PSWE_MINMB") ? atoi(getenv("PSWE_MINMB")) : 24;
+  const int minph = std::max<int>(minph_floor, (int)(((size_t)minmb << 20) / (per_phase * sizeof(double2))));
   int nchunks = std::max((P + cpmax - 1) / cpmax, std::min(c->n_lanes, P / minph));
   const int lanes = std::max(1, std::min(c->n_lanes, nchunks));
   nchunks = (nchunks + lanes - 1) / lanes * lanes;
@@ -626,7 +713,7 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
     // a single slot (one chunk, Gc = 1, e.g. the fine-step reference's one
     // node) is the output itself: pass C writes it, no reduction launch
     double2* sl = direct ? Ac : c->slots.p + (size_t)L * Gc * cw;
-    TRY(dispatchA(c, ph, p0, np, Uc, I1, gate_bit >= 0 ? c->hgate.p + 4 : nullptr, lst[L]));
+    TRY(dispatchA(c, ph, p0, np, Uc, I1, gate ? c->hgate.p + 4 : nullptr, lst[L]));
     TRY(dispatchB(c, np, lanes, mrow[L], mcol[L], I2, lst[L]));
     TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
   }
@@ -641,12 +728,6 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
                 Ac));
     c->launches++;
     c->variant[PSWE_V_REDUCE]++;
-    CU(cudaGetLastError());
-  }
-  if (gate_bit >= 0) {
-    CU(launch_k(c->pdl, herm_eval_kernel, 1, 256, 0, st, c->hgate.p, c->bdef, c->hgate.p + 4, P, c->H, c->g,
-                c->flags.p, gate_bit));
-    c->launches++;
     CU(cudaGetLastError());
   }
   return PSWE_OK;
@@ -790,29 +871,30 @@ int step_impl_w(pswe_ctx* c, const PhaseSet& ps, double dt, Full3 U, Full3w out,
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, U.u, U.v, U.e, Uc, c->hgate.p, W, ws));
   c->launches++;
-  TRY(rhs_compact(c, ps, Uc, Ac, st, HERM_BIT0));
+  TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)Ac, edt, u1, c->flags.p, W, ws));
+  CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)Ac, edt, u1, c->flags.p, W, ws,
+              hgate_of(c, ps.P, HERM_BIT0)));
   c->launches++;
   // stage 2
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, (const double2*)u1.u, (const double2*)u1.v,
               (const double2*)u1.e, Uc, c->hgate.p, W, ws));
   c->launches++;
-  TRY(rhs_compact(c, ps, Uc, Ac, st, HERM_BIT0 + 1));
+  TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage2_kernel, gb, 256, 0, st, G, pr, dt, U, f3c(u1), (const double2*)Ac, u2, c->flags.p, W,
-              ws));
+              ws, hgate_of(c, ps.P, HERM_BIT0 + 1)));
   c->launches++;
   // stage 3
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, (const double2*)u2.u, (const double2*)u2.v,
               (const double2*)u2.e, Uc, c->hgate.p, W, ws));
   c->launches++;
-  TRY(rhs_compact(c, ps, Uc, Ac, st, HERM_BIT0 + 2));
+  TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage3_kernel, gb, 256, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)Ac, out,
-              c->flags.p, W, ws));
+              c->flags.p, W, ws, hgate_of(c, ps.P, HERM_BIT0 + 2)));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -1157,7 +1239,7 @@ int pswe_unpack(pswe_ctx* c, const double* Uc, double* u, double* v, double* e, 
   if (!c || !u || !v || !e || !Uc) return set_err(PSWE_EINVAL, "null argument");
   CU(cudaSetDevice(c->device));
   unpack_kernel<<<elem_grid(c, c->full_elems()), 256, 0, (cudaStream_t)stream>>>(
-      c->grid(), (const double2*)Uc, (double2*)u, (double2*)v, (double2*)e, 1, (size_t)0);
+      c->grid(), (const double2*)Uc, (double2*)u, (double2*)v, (double2*)e, 1, (size_t)0, no_gate());
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;
@@ -1187,8 +1269,12 @@ static int gated_rhs(pswe_ctx* c, const double* u, const double* v, const double
                                                                (size_t)0);
   c->launches++;
   CU(cudaGetLastError());
-  TRY(rhs_compact(c, ps, c->Uc.p, c->Ac.p, st, HERM_BIT_RHS));
-  TRY(pswe_unpack(c, (const double*)c->Ac.p, du, dv, de, st));
+  TRY(rhs_compact(c, ps, c->Uc.p, c->Ac.p, st, true));
+  unpack_kernel<<<elem_grid(c, c->full_elems()), 256, 0, st>>>(c->grid(), (const double2*)c->Ac.p, (double2*)du,
+                                                              (double2*)dv, (double2*)de, 1, (size_t)0,
+                                                              hgate_of(c, ps.P, HERM_BIT_RHS));
+  c->launches++;
+  CU(cudaGetLastError());
   CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   if (*c->flags_host & (1 << HERM_BIT_RHS)) return exact_gate(c, ps.s, s_host, k, f3(u, v, e), st);

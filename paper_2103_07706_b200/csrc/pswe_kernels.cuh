@@ -52,6 +52,43 @@ __device__ __forceinline__ double abs2(double2 a) { return fma(a.x, a.x, a.y * a
 // must not drop a non-finite value the way fmax does
 __device__ __forceinline__ double nanmax(double a, double b) { return (a > b || a != a) ? a : b; }
 
+// The Hermitian gate's fast verdict (herm_kernels.cuh), evaluated by block 0
+// of the kernel that consumes an evaluation's result: flags bit `bit` when
+// some phase might fail the gate, and resets the statistics (hstat[3] = max
+// |D_f|^2 of the packed input, pscale[P] = per-phase max squared magnitude)
+// for the next evaluation.  bit < 0: no gate.
+struct HermGate {
+  double* hstat;
+  double* pscale;
+  int P;
+  double bdef, H, g;
+  int* flags;
+  int bit;
+};
+
+__device__ void herm_eval_block(const HermGate& hg) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  const double dW2 = hg.H * hg.hstat[0] + hg.H * hg.hstat[1] + hg.g * hg.hstat[2];
+  const double d = sqrt(dW2) / sqrt(fmin(hg.H, hg.g)) + hg.bdef;
+  int mine = 0;
+  if (d != 0.0) {  // an exactly Hermitian input cannot fail
+    for (int p = threadIdx.x; p < hg.P; p += blockDim.x) {
+      const double sc = sqrt(hg.pscale[p]);
+      // NaN anywhere makes the test false: flagged, the exact path decides
+      if (!(1.01 * d < 1e-12 * (sc - 0.5 * d))) mine = 1;
+    }
+  }
+  if (mine) bad = 1;
+  __syncthreads();  // every read precedes the resets
+  for (int p = threadIdx.x; p < hg.P; p += blockDim.x) hg.pscale[p] = 0.0;
+  if (threadIdx.x == 0) {
+    hg.hstat[0] = hg.hstat[1] = hg.hstat[2] = 0.0;
+    if (bad) atomicOr(hg.flags, 1 << hg.bit);
+  }
+}
+
 struct PhaseDev {
   const double* s;  // [P] live node shifts, ascending k
   const double* w;  // [P] weights
@@ -1121,9 +1158,10 @@ __device__ __forceinline__ C3 compact_at(const GridDev& G, const double2* __rest
 }
 
 __global__ void unpack_kernel(GridDev G, const double2* __restrict__ Ac, double2* __restrict__ u,
-                              double2* __restrict__ v, double2* __restrict__ e, int W, size_t ws) {
+                              double2* __restrict__ v, double2* __restrict__ e, int W, size_t ws, HermGate hg) {
   griddep_wait();
   griddep_launch();
+  if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
   const size_t n = (size_t)G.nx * G.ny, cs = 3 * (size_t)G.Ky * G.Kx;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < (size_t)W * n;
        t += (size_t)gridDim.x * blockDim.x) {
@@ -1190,9 +1228,11 @@ __device__ __forceinline__ Full3w wshift(const Full3w& a, size_t o) { return {a.
 
 // stage 1 (integrator.py:96-98): e_dt = E(dt) U;  u1 = e_dt + dt * E(dt) A(U)
 __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const double2* __restrict__ Ac,
-                              Full3w edt, Full3w u1, int* flags, int W, size_t ws) {
+                              Full3w edt, Full3w u1, int* flags, int W, size_t ws,
+                              HermGate hg) {
   griddep_wait();
   griddep_launch();
+  if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
   const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
     const size_t t = i0 + threadIdx.x;
@@ -1213,9 +1253,11 @@ __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const doub
 
 // stage 2 (integrator.py:99-100): u2 = 3/4 E(dt/2) U + 1/4 E(-dt/2) (u1 + dt A(u1))
 __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, const double2* __restrict__ Ac,
-                              Full3w u2, int* flags, int W, size_t ws) {
+                              Full3w u2, int* flags, int W, size_t ws,
+                              HermGate hg) {
   griddep_wait();
   griddep_launch();
+  if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
   const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   const double h = 0.5 * dt;
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
@@ -1237,9 +1279,11 @@ __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, 
 
 // stage 3 (integrator.py:101-102): out = 1/3 e_dt + 2/3 E(dt/2) (u2 + dt A(u2))
 __global__ void stage3_kernel(GridDev G, Prop pr, double dt, Full3 edt, Full3 u2, const double2* __restrict__ Ac,
-                              Full3w out, int* flags, int W, size_t ws) {
+                              Full3w out, int* flags, int W, size_t ws,
+                              HermGate hg) {
   griddep_wait();
   griddep_launch();
+  if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
   const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   const double h = 0.5 * dt;
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {

@@ -529,6 +529,16 @@ def test_poisoned_scratch_gives_the_same_bits(tmp_path):
         "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
         "s = pk.run(c.state, cfg, c.params, t_end=4 * c.dt).states[-1]\n"
         "outs.append(np.stack([s.u, s.v, s.eta]))\n"
+        "g = pk.make_grid(64, 32, 4.0e7, 2.0e7)\n"
+        "rng = np.random.default_rng(9)\n"
+        "f = lambda sc: pk.dealias(g, pk.to_spectral(g, sc * rng.standard_normal((64, 32))))\n"
+        "st = pk.State(grid=g, u=f(1.0), v=f(1.0), eta=f(50.0))\n"
+        "p = pk.PhysicsParams(f=1e-4, g=9.8, H=5960.0, b=np.zeros((64, 32), complex))\n"
+        "ctx = pk.dynamics.context(st, p)\n"
+        "for _ in range(2):\n"
+        "    a = pk.averaged_tendency(st, pk.kernel_weights(3600.0, 256), p, pk.PropagatorSpec.exact())\n"
+        "    outs.append(np.stack([a.u, a.v, a.eta]))\n"
+        "for k, v in ctx.variant_launches.items(): var[k] = var.get(k, 0) + v\n"
         "np.savez(sys.argv[1], *outs)\n"
         "print(json.dumps(var))\n" % str(ROOT))
     base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
@@ -541,8 +551,61 @@ def test_poisoned_scratch_gives_the_same_bits(tmp_path):
         var = json.loads(p.stdout.strip().splitlines()[-1])
         with np.load(f) as z:
             res.append([z[k] for k in z.files])
-    for name in ("passB_split", "passB_row", "passB_pair", "reduce"):
+    for name in ("passB_split", "passB_row", "passB_pair", "reduce", "fused"):
         assert var[name] > 0, (name, var)
     for a, b in zip(res[0], res[1]):
         assert np.all(np.isfinite(b))
         assert np.array_equal(a, b)
+
+
+def test_fused_small_grid_kernel_matches_three_pass_path(tmp_path):
+    """n <= 64: the one-CTA-per-phase-group kernel (fused_kernels.cuh) vs the
+    three-pass pipeline (PSWE_NO_FUSED) -- same transforms and formulas, so
+    equal to round-off -- and vs the oracle, at every small size, one and
+    many phases per CTA, a window batch and the stepper."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys, json, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2103_07706_b200 as pk\n"
+        "from paper_2103_07706_b200 import cases\n"
+        "outs = []\n"
+        "for r, M in ((1, 4), (2, 8), (3, 8), (3, 64), (3, 256)):\n"
+        "    c = cases.case_c5(r, M)\n"
+        "    a = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())\n"
+        "    outs.append(np.stack([a.u, a.v, a.eta]))\n"
+        "c = cases.case_c1()\n"
+        "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
+        "s = pk.run(c.state, cfg, c.params, t_end=3 * c.dt).states[-1]\n"
+        "outs.append(np.stack([s.u, s.v, s.eta]))\n"
+        "res = pk.window_sweep(c.state, c.params, c.dt, 2 * c.dt, [0.0, 1800.0, 3600.0], M=8)\n"
+        "outs += [np.stack([r.final.u, r.final.v, r.final.eta]) for r in res]\n"
+        "np.savez(sys.argv[1], *outs)\n"
+        "print(json.dumps(pk.dynamics.context(c.state, c.params).variant_launches))\n" % str(ROOT))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
+    res, var = [], []
+    for i, env in enumerate(({}, {"PSWE_NO_FUSED": "1"})):
+        f = tmp_path / f"f{i}.npz"
+        p = subprocess.run([sys.executable, "-c", code, str(f)], env={**base, **env},
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr
+        var.append(json.loads(p.stdout.strip().splitlines()[-1]))
+        with np.load(f) as z:
+            res.append([z[k] for k in z.files])
+    assert var[0]["fused"] > 0 and var[1]["fused"] == 0
+    for a, b in zip(res[0], res[1]):
+        assert rel_l2(a, b) <= 1e-13
+    # and the fused results against the oracle at 32^2 / M = 128 (unbalanced state)
+    c = cases.case_c5(3, 128)
+    g = c.grid
+    rng = np.random.default_rng(11)
+    S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, c.params.f, c.params.g, c.params.H)
+    U = arr(c.state) + np.stack([O.truncate(O.spectral(sc * rng.standard_normal((32, 32))), S.mask)
+                                 for sc in (1.0, 1.0, 50.0)])
+    got = pk.averaged_tendency(state_from(U, g), c.quadrature, c.params, pk.PropagatorSpec.exact())
+    assert O.rel_l2(arr(got), O.averaged_tendency(S, U, c.quadrature.s, c.quadrature.w, workers=8)) <= RHS_TOL
