@@ -238,6 +238,42 @@ cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, si
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and
+// device (it costs microseconds per call on the latency-bound small sizes)
+std::mutex g_attr_mutex;
+std::vector<std::pair<const void*, int>> g_attr_done;
+template <typename K>
+cudaError_t smem_attr(K kern, size_t smem, int device) {
+  std::lock_guard<std::mutex> lock(g_attr_mutex);
+  const void* key = reinterpret_cast<const void*>(kern);
+  for (const auto& e : g_attr_done)
+    if (e.first == key && e.second == device) return cudaSuccess;
+  const cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (r == cudaSuccess) g_attr_done.emplace_back(key, device);
+  return r;
+}
+
+// resident CTAs per SM of a kernel (occupancy query, cached per kernel / device)
+struct OccKey {
+  const void* k;
+  int device, threads;
+  size_t smem;
+  int per_sm;
+};
+std::vector<OccKey> g_occ;
+template <typename K>
+int occupancy(K kern, int threads, size_t smem, int device, int fallback) {
+  std::lock_guard<std::mutex> lock(g_attr_mutex);
+  const void* key = reinterpret_cast<const void*>(kern);
+  for (const auto& e : g_occ)
+    if (e.k == key && e.device == device && e.threads == threads && e.smem == smem) return e.per_sm;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = fallback;
+  g_occ.push_back({key, device, threads, smem, per_sm});
+  return per_sm;
+}
+
 bool pdl_enabled() {
   static const bool off = getenv("PSWE_NO_PDL") != nullptr;  // A/B switch
   return !off;
@@ -250,7 +286,7 @@ int launchA(pswe_ctx* c, const PhaseDev& ph, int p0, int np, const double2* Uc, 
   using W = PassAW<NX, MW>;
   const size_t smem = W::bytes(c->Kx);
   auto kern = passA_kernel<NX, MW>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(smem_attr(kern, smem, c->device));
   const int nblk = ((np + 1) / 2) * ((c->Ky + W::GPW - 1) / W::GPW);
   const int blocks = std::min(nblk, W::CTAS * c->sms);
   ProfScope ps(c, 0, st);
@@ -272,7 +308,7 @@ int launchB_small(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cuda
   using W = PassBW<NY>;
   const size_t smem = W::template bytes<false>();
   auto kern = passB_kernel<NY>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(smem_attr(kern, smem, c->device));
   const int blocks = (np * c->nx + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
   CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), np, mI1, I2));
@@ -287,7 +323,7 @@ int launchB_split(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cuda
   using W = PassBSW<NY>;
   const size_t smem = W::bytes();
   auto kern = passB_split_kernel<NY>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(smem_attr(kern, smem, c->device));
   const int blocks = (np * c->nx + W::GPW - 1) / W::GPW;
   ProfScope ps(c, 1, st);
   CU(launch_k(c->pdl, kern, blocks, 128, smem, st, c->grid(), np, mI1, I2));
@@ -302,7 +338,7 @@ int launchB_pair(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap&
   using W = PassBW<NY>;
   const size_t smem = W::template bytes<true>();
   auto kern = passB_pair_kernel<NY>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(smem_attr(kern, smem, c->device));
   const int ntp = ((np + 1) / 2) * c->nx;
   const int blocks = (ntp + W::GPC - 1) / W::GPC;
   ProfScope ps(c, 1, st);
@@ -343,11 +379,9 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
   // of the resident CTAs (occupancy query), each CTA keeping >= 4 phases to amortise its
   // prologue and slot update.  Pick the Gc with the best wave efficiency.
   const int cols = (c->Ky + PassCW<NX>::GPW - 1) / PassCW<NX>::GPW;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, passC_kernel<NX, false>, PassCW<NX>::WARPS * 32,
-                                                    PassCW<NX>::bytes(c->Kx)) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 3;
+  smem_attr(passC_kernel<NX, false>, PassCW<NX>::bytes(c->Kx), c->device);  // before the occupancy query
+  const int per_sm = occupancy(passC_kernel<NX, false>, PassCW<NX>::WARPS * 32, PassCW<NX>::bytes(c->Kx),
+                               c->device, 3);
   const int sms = c->sms;
   const int slots = per_sm * sms;
   int best = 1;
@@ -374,7 +408,7 @@ int launchC(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, 
   using W = PassCW<NX>;
   const size_t smem = W::bytes(c->Kx);
   auto kern = passC_kernel<NX, MW>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(smem_attr(kern, smem, c->device));
   const int cols = (c->Ky + W::GPW - 1) / W::GPW;
   const int blocks = cols * Gc;
   ProfScope ps(c, 2, st);
@@ -557,7 +591,7 @@ int launch_fused(pswe_ctx* c, const PhaseDev& ph, int Gc, const double2* Uc, dou
                  cudaStream_t st) {
   using W = FusedW<N>;
   auto kern = fused_kernel<N, MW>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::bytes()));
+  CU(smem_attr(kern, W::bytes(), c->device));
   ProfScope ps(c, 0, st);
   CU(launch_k(c->pdl, kern, Gc, W::NT, W::bytes(), st, c->grid(), c->prop(), ph, Gc, Uc, c->ctab_cur, out, pscale));
   c->launches++;
@@ -568,12 +602,8 @@ int launch_fused(pswe_ctx* c, const PhaseDev& ph, int Gc, const double2* Uc, dou
 
 template <int N>
 int fused_capacity(const pswe_ctx* c) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<N, false>, FusedW<N>::NT,
-                                                    FusedW<N>::bytes()) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  return per_sm * c->sms;
+  smem_attr(fused_kernel<N, false>, FusedW<N>::bytes(), c->device);  // before the occupancy query
+  return occupancy(fused_kernel<N, false>, FusedW<N>::NT, FusedW<N>::bytes(), c->device, 1) * c->sms;
 }
 
 // Measured (tools/fused_check.py): n <= 32 one CTA per phase group wins
