@@ -20,6 +20,7 @@
 #include "diag_kernels.cuh"
 #include "herm_kernels.cuh"
 #include "fused_kernels.cuh"
+#include "generic_kernels.cuh"
 
 using namespace pswe;
 
@@ -90,6 +91,8 @@ struct DevBuf {
 
 struct pswe_ctx {
   int device = 0;
+  bool gen = false;        // not a power of two <= 512: the generic kernels (generic_kernels.cuh)
+  FftPlan plx{}, ply{};    // their radix plans
   int sms = 148;  // multiprocessor count of the device (queried at create)
   int nx = 0, ny = 0, kxm = 0, kym = 0, Kx = 0, Ky = 0;
   double Lx = 0, Ly = 0, f = 0, g = 0, H = 0;
@@ -241,15 +244,25 @@ cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, si
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and
 // device (it costs microseconds per call on the latency-bound small sizes)
 std::mutex g_attr_mutex;
-std::vector<std::pair<const void*, int>> g_attr_done;
+struct AttrKey {
+  const void* k;
+  int device;
+  size_t smem;  // the largest maximum set so far (the attribute is an upper bound)
+};
+std::vector<AttrKey> g_attr_done;
 template <typename K>
 cudaError_t smem_attr(K kern, size_t smem, int device) {
   std::lock_guard<std::mutex> lock(g_attr_mutex);
   const void* key = reinterpret_cast<const void*>(kern);
-  for (const auto& e : g_attr_done)
-    if (e.first == key && e.second == device) return cudaSuccess;
+  for (auto& e : g_attr_done)
+    if (e.k == key && e.device == device) {
+      if (smem <= e.smem) return cudaSuccess;
+      const cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (r == cudaSuccess) e.smem = smem;
+      return r;
+    }
   const cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (r == cudaSuccess) g_attr_done.emplace_back(key, device);
+  if (r == cudaSuccess) g_attr_done.push_back({key, device, smem});
   return r;
 }
 
@@ -585,6 +598,62 @@ PhaseSet batch_phases(pswe_ctx* c) {
   return {c->bs_dev.p, c->bw_dev.p, c->bwin_dev.p, (int)c->b_s.size(), c->bW, &c->ctab_b, &c->ctab_b_valid};
 }
 
+// ---- generic sizes (generic_kernels.cuh): any even n, also n > 512
+FftPlan make_plan(int n, const double2* tw) {
+  FftPlan p{};
+  p.n = n;
+  p.tw = tw;
+  int m = n;
+  while (m % 4 == 0 && p.nf < GEN_MAX_FACTORS) { p.f[p.nf++] = 4; m /= 4; }
+  for (int r : {2, 3, 5, 7})
+    while (m % r == 0 && p.nf < GEN_MAX_FACTORS) { p.f[p.nf++] = r; m /= r; }
+  for (int r = 11; m > 1 && p.nf < GEN_MAX_FACTORS; r += 2)
+    while (m % r == 0) { p.f[p.nf++] = r; m /= r; }
+  return p;
+}
+
+int gen_groups(const pswe_ctx* c, int CP) {
+  // pass C: Ky columns x Gc phase groups, about two waves of 4 CTAs per SM, >= 2 phases each
+  const int want = std::max(1, (8 * c->sms + c->Ky - 1) / c->Ky);
+  return std::max(1, std::min(want, std::max(1, CP / 2)));
+}
+
+int launch_gen(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* Uc, double2* I1,
+               double2* I2, double2* slots, double* pscale, cudaStream_t st) {
+  const size_t sA = ((size_t)3 * c->Kx + 2 * (size_t)c->nx) * sizeof(double2);
+  const size_t sB = (size_t)6 * c->ny * sizeof(double2);
+  const size_t sC = ((size_t)7 * c->Kx + 2 * (size_t)c->nx) * sizeof(double2);
+  CU(smem_attr(gen_passA_kernel, sA, c->device));
+  CU(smem_attr(gen_passB_kernel, sB, c->device));
+  CU(smem_attr(gen_passC_kernel<false>, sC, c->device));
+  CU(smem_attr(gen_passC_kernel<true>, sC, c->device));
+  {
+    ProfScope ps(c, 0, st);
+    CU(launch_k(c->pdl, gen_passA_kernel, np * c->Ky, GEN_THREADS, sA, st, c->grid(), c->prop(), ph, p0, np, Uc,
+                c->ctab_cur, I1, c->plx, pscale));
+  }
+  {
+    ProfScope ps(c, 1, st);
+    CU(launch_k(c->pdl, gen_passB_kernel, np * c->nx, GEN_THREADS, sB, st, c->grid(), np, (const double2*)I1, I2,
+                c->ply));
+  }
+  {
+    ProfScope ps(c, 2, st);
+    if (ph.win)
+      CU(launch_k(c->pdl, gen_passC_kernel<true>, c->Ky * Gc, GEN_THREADS, sC, st, c->grid(), c->prop(), ph, p0, np,
+                  Gc, (const double2*)I2, c->ctab_cur, slots, first, c->plx));
+    else
+      CU(launch_k(c->pdl, gen_passC_kernel<false>, c->Ky * Gc, GEN_THREADS, sC, st, c->grid(), c->prop(), ph, p0,
+                  np, Gc, (const double2*)I2, c->ctab_cur, slots, first, c->plx));
+  }
+  c->launches += 3;
+  c->variant[PSWE_V_PASSA]++;
+  c->variant[PSWE_V_PASSB_ROW]++;
+  c->variant[PSWE_V_PASSC]++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
 // Small square grids: the one-CTA-per-phase-group kernel (fused_kernels.cuh)
 template <int N, bool MW>
 int launch_fused(pswe_ctx* c, const PhaseDev& ph, int Gc, const double2* Uc, double2* out, double* pscale,
@@ -613,7 +682,7 @@ int fused_capacity(const pswe_ctx* c) {
 bool fused_ok(const pswe_ctx* c) {
   static const bool off = getenv("PSWE_NO_FUSED") != nullptr;  // A/B switch
   static const bool f64 = getenv("PSWE_FUSED64") != nullptr;
-  return !off && c->nx == c->ny && (c->nx <= 32 || (f64 && c->nx == 64));
+  return !off && !c->gen && c->nx == c->ny && (c->nx <= 32 || (f64 && c->nx == 64));
 }
 
 // `gate`: the input was packed with the gate's statistics (pack_kernel
@@ -704,7 +773,7 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
   nchunks = (nchunks + lanes - 1) / lanes * lanes;
   const int CP = std::max(1, std::min(P, (P + nchunks - 1) / nchunks));
   nchunks = (P + CP - 1) / CP;
-  const int Gc = groupsC(c, CP);  // accumulation slots = phase groups per chunk
+  const int Gc = c->gen ? gen_groups(c, CP) : groupsC(c, CP);  // accumulation slots = phase groups per chunk
   c->pdl = pdl_enabled() && nchunks == 1;
   const size_t cw = (size_t)ps.W * c->compact_elems();  // one slot set: W compact states
   TRY(c->inter.alloc(per_phase * CP * lanes));
@@ -724,7 +793,7 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
   ph.ustride = c->compact_elems();
   cudaStream_t lst[pswe_ctx::MAX_LANES] = {st, c->st_lane[0], c->st_lane[1], c->st_lane[2]};
   CUtensorMap mrow[pswe_ctx::MAX_LANES], mcol[pswe_ctx::MAX_LANES];
-  for (int L = 0; L < lanes; ++L) {
+  for (int L = 0; L < lanes && !c->gen; ++L) {
     double2* I1 = c->inter.p + (size_t)L * per_phase * CP;
     TRY(map_rows_I1(c, I1, CP, &mrow[L]));
     TRY(map_tiles_I2(c, I1 + (size_t)5 * c->Ky * c->nx * CP, CP, &mcol[L]));
@@ -743,6 +812,11 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
     // a single slot (one chunk, Gc = 1, e.g. the fine-step reference's one
     // node) is the output itself: pass C writes it, no reduction launch
     double2* sl = direct ? Ac : c->slots.p + (size_t)L * Gc * cw;
+    if (c->gen) {
+      TRY(launch_gen(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, Uc, I1, I2, sl, gate ? c->hgate.p + 4 : nullptr,
+                     lst[L]));
+      continue;
+    }
     TRY(dispatchA(c, ph, p0, np, Uc, I1, gate ? c->hgate.p + 4 : nullptr, lst[L]));
     TRY(dispatchB(c, np, lanes, mrow[L], mcol[L], I2, lst[L]));
     TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
@@ -1042,9 +1116,8 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
   if (!(Ly > 0)) return set_err(PSWE_EINVAL, "Ly must be positive, got %g", Ly);
   if (!(g > 0)) return set_err(PSWE_EINVAL, "g must be positive, got %g", g);
   if (!(H > 0)) return set_err(PSWE_EINVAL, "H must be positive, got %g", H);
-  if (!pow2_ok(nx) || !pow2_ok(ny))
-    return set_err(PSWE_EUNSUPPORTED,
-                   "grid %dx%d not supported by the B200 path (nx, ny must be powers of two in [8, 512])", nx, ny);
+  if (nx > 4096 || ny > 4096)
+    return set_err(PSWE_EUNSUPPORTED, "grid %dx%d not supported by the B200 path (nx, ny <= 4096)", nx, ny);
   CU(cudaSetDevice(device));
   pswe_ctx* c = new pswe_ctx();
   c->device = device;
@@ -1096,6 +1169,9 @@ int pswe_create(pswe_ctx** out, int nx, int ny, double Lx, double Ly, double f, 
   }
   twiddle_kernel<<<(nx + 255) / 256, 256>>>(c->twx.p, nx);
   twiddle_kernel<<<(ny + 255) / 256, 256>>>(c->twy.p, ny);
+  c->gen = !pow2_ok(nx) || !pow2_ok(ny);
+  c->plx = make_plan(nx, c->twx.p);
+  c->ply = make_plan(ny, c->twy.p);
   cudaMemset(c->bc.p, 0, (size_t)c->Ky * c->Kx * sizeof(double2));
   cudaMemset(c->flags.p, 0, sizeof(int));
   {
@@ -1671,6 +1747,18 @@ static int physical_fields(pswe_ctx* c, const double* u, const double* v, const 
   TRY(c->diag_cols.alloc((size_t)4 * (c->ny / 2 + 1) * c->nx));
   TRY(c->diag_part.alloc((size_t)3 * c->nx));
   const double2 *U = (const double2*)u, *V = (const double2*)v, *E = (const double2*)e;
+  if (c->gen) {
+    const size_t sc = (size_t)2 * c->nx * sizeof(double2), sr = (size_t)4 * c->ny * sizeof(double2);
+    CU(smem_attr(gen_diag_cols_kernel, sc, c->device));
+    CU(smem_attr(gen_diag_rows_kernel, sr, c->device));
+    gen_diag_cols_kernel<<<4 * (c->ny / 2 + 1), GEN_THREADS, sc, st>>>(c->grid(), U, V, E, c->bfull.p,
+                                                                        c->diag_cols.p, c->plx);
+    gen_diag_rows_kernel<<<c->nx, GEN_THREADS, sr, st>>>(c->grid(), c->diag_cols.p, c->H, c->g, c->diag_part.p,
+                                                          phys, c->ply);
+    c->launches += 2;
+    CU(cudaGetLastError());
+    return PSWE_OK;
+  }
   int rc = PSWE_EUNSUPPORTED;
   switch (c->nx) {
     case 8: rc = launch_diag_cols<8>(c, U, V, E, c->bfull.p, st); break;

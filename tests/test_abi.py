@@ -41,7 +41,7 @@ def test_invalid_arguments_fail_without_a_gpu():
     # argument validation happens before any CUDA call
     assert lib.pswe_create(ctypes.byref(h), 6, 8, 1.0, 1.0, 1e-4, 9.8, 1.0, 0) == _native.PSWE_EINVAL
     assert b"nx must be even and >= 8" in lib.pswe_last_error()
-    assert lib.pswe_create(ctypes.byref(h), 48, 48, 1.0, 1.0, 1e-4, 9.8, 1.0, 0) == _native.PSWE_EUNSUPPORTED
+    assert lib.pswe_create(ctypes.byref(h), 8192, 48, 1.0, 1.0, 1e-4, 9.8, 1.0, 0) == _native.PSWE_EUNSUPPORTED
     assert lib.pswe_create(ctypes.byref(h), 32, 32, 1.0, 1.0, 1e-4, -9.8, 1.0, 0) == _native.PSWE_EINVAL
     assert b"g must be positive" in lib.pswe_last_error()
 

@@ -285,9 +285,47 @@ def test_output_is_band_limited_and_hermitian():
     assert np.max(np.abs(got - np.conj(refl))) <= 1e-13 * np.max(np.abs(got))
 
 
-def test_unsupported_grid_is_refused():
-    g = pk.make_grid(48, 48, 4.0e7, 4.0e7)
-    st = pk.State(grid=g, u=np.zeros((48, 48)), v=np.zeros((48, 48)), eta=np.zeros((48, 48)))
+@pytest.mark.parametrize("nx,ny,M", [(12, 12, 3), (48, 48, 8), (96, 96, 16), (48, 96, 4), (30, 18, 2), (1024, 1024, 2)])
+def test_any_even_grid_matches_oracle(nx, ny, M):
+    """Every even n >= 8 the reference accepts (grid.py:91-93): the generic
+    mixed-radix kernels (3 * 2^k, other primes, n > 512) vs the oracle, for
+    N alone and the averaged tendency, with topography."""
+    rng = np.random.default_rng(nx + ny)
+    g = pk.make_grid(nx, ny, 4.0e7, 4.0e7 * ny / nx)
+    S = O.Setup(nx, ny, g.Lx, g.Ly, F0, G0, H0)
+    S.b = O.truncate(O.spectral(30.0 * rng.standard_normal((nx, ny))), S.mask)
+    U = np.stack([O.truncate(O.spectral(sc * rng.standard_normal((nx, ny))), S.mask) for sc in (1.0, 1.0, 50.0)])
+    p = pk.PhysicsParams(f=F0, g=G0, H=H0, b=S.b)
+    st = state_from(U, g)
+    assert O.rel_l2(arr(pk.apply_nonlinear(st, p)), O.nonlinear(S, U)) <= 1e-12
+    q = pk.kernel_weights(3600.0, M)
+    got = pk.averaged_tendency(st, q, p, pk.PropagatorSpec.exact())
+    assert O.rel_l2(arr(got), O.averaged_tendency(S, U, q.s, q.w, workers=8)) <= RHS_TOL
+
+
+def test_any_even_grid_steps_run_and_diagnostics():
+    """48^2 (3 * 2^4): a 3-step run vs the oracle, its snapshot diagnostics vs
+    the oracle's, and the 12^2 grid of the reference's own tests through a step."""
+    for n, steps in ((48, 3), (12, 2)):
+        rng = np.random.default_rng(n)
+        g = pk.make_grid(n, n, 4.0e7, 4.0e7)
+        S = O.Setup(n, n, g.Lx, g.Ly, F0, G0, H0)
+        U = np.stack([O.truncate(O.spectral(sc * rng.standard_normal((n, n))), S.mask) for sc in (1.0, 1.0, 50.0)])
+        p = flat(g)
+        st = state_from(U, g)
+        q = pk.kernel_weights(1800.0, 4)
+        cfg = pk.StepConfig(dt=900.0, quadrature=q, propagator_spec=pk.PropagatorSpec.exact())
+        traj = pk.run(st, cfg, p, t_end=steps * 900.0)
+        want = O.run(S, U, 900.0, steps, q.s, q.w)
+        assert O.rel_l2(arr(traj.states[-1]), want) <= STEP_TOL
+        en, ms = O.energy_mass(S, want)
+        assert abs(traj.energy[-1] - en) <= 1e-12 * abs(en)
+        assert abs(traj.mass[-1] - ms) <= 1e-12 * abs(ms)
+
+
+def test_oversized_grid_is_refused():
+    g = pk.make_grid(8192, 8, 4.0e7, 4.0e7)
+    st = pk.State(grid=g, u=np.zeros((8192, 8)), v=np.zeros((8192, 8)), eta=np.zeros((8192, 8)))
     with pytest.raises(ValueError, match="not supported by the B200 path"):
         pk.apply_nonlinear(st, flat(g))
 
