@@ -300,7 +300,9 @@ def run_reference(args, ws, rank):
     threads = cpu_threads()
     prob = R.problem(case)
     if prob is not None:
-        m = max(1, min(case.M - 1, threads))
+        # about eight phases per host thread per step (the full evaluation's
+        # thread efficiency at a fraction of its 7-10 s)
+        m = max(1, min(case.M - 1, 4 * threads))
         quad = prob.sub_quadrature(m)
         per_step = int(np.count_nonzero(quad.w))
         for _ in range(args.warmup):
