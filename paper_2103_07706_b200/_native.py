@@ -333,6 +333,8 @@ class Context:
         self._prop_key = None
         self._b_copy = None
         self._b_obj = None
+        self._quad_src = None  # the (s, w) array objects last pushed
+        self._spec_obj = None  # the PropagatorSpec last configured (propagator.configure)
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -378,6 +380,7 @@ class Context:
         _check(_lib.pswe_set_lanes(self.h, int(lanes)))
 
     def set_quadrature(self, s: np.ndarray, w: np.ndarray) -> None:
+        self._quad_src = (s, w)
         s = np.ascontiguousarray(s, dtype=np.float64)
         w = np.ascontiguousarray(w, dtype=np.float64)
         key = (s.tobytes(), w.tobytes())
@@ -389,6 +392,7 @@ class Context:
 
     def set_propagator(self, kind: str, Lambda: float = 0.0, n_poly: int = 1,
                        a: np.ndarray | None = None) -> None:
+        self._spec_obj = None  # propagator.configure records the spec object after this
         key = (kind, float(Lambda), int(n_poly))
         if key == self._prop_key:
             return

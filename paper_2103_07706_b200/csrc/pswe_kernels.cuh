@@ -175,8 +175,10 @@ struct PassAW {
   // add u, v, eta of phase q's window in slots 6..8 when it differs from p's)
   // | xbuf per group
   static constexpr int SLOTS = MW ? 9 : 6;
+  // ... | the Hermitian gate's per-warp phase maxima [WARPS][2]
   static size_t bytes(int Kx) {
-    return 16 + (size_t)GPW * SLOTS * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double);
+    return 16 + (size_t)GPW * SLOTS * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) +
+           (size_t)WARPS * 2 * sizeof(double);
   }
 };
 
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
   double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [SLOTS][GPW][Kx]
   double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * W::SLOTS * Kx);
+  double* gred = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;  // [WARPS][2]
   const bool tab = ctab != nullptr;
   const int cols = (Ky + GPW - 1) / GPW;
   const int npair = (np + 1) / 2;
@@ -287,27 +290,37 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
         o[0] = cscale(G.inv_n2, q.u);
         o[fs] = cscale(G.inv_n2, q.v);
         o[2 * fs] = cscale(G.inv_n2, dep);
-        if (pscale) {
-          const double m = nanmax(nanmax(abs2(q.u), abs2(q.v)), abs2(dep));
-          if (sub) gmax1 = nanmax(m, gmax1);
-          else gmax0 = nanmax(m, gmax0);
+        if (pscale) {  // (a non-finite input is flagged through pack's statistics: fmax is enough here)
+          const double m = fmax(fmax(abs2(q.u), abs2(q.v)), abs2(dep));
+          if (sub) gmax1 = fmax(m, gmax1);
+          else gmax0 = fmax(m, gmax0);
         }
       }
     }
     if (pscale) {
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
-        gmax0 = nanmax(gmax0, __shfl_xor_sync(0xffffffffu, gmax0, o));
-        gmax1 = nanmax(gmax1, __shfl_xor_sync(0xffffffffu, gmax1, o));
+        gmax0 = fmax(gmax0, __shfl_xor_sync(0xffffffffu, gmax0, o));
+        gmax1 = fmax(gmax1, __shfl_xor_sync(0xffffffffu, gmax1, o));
       }
       if (lane == 0) {
-        unsigned long long* ps = reinterpret_cast<unsigned long long*>(pscale + p0 + pa);
-        atomicMax(ps, (unsigned long long)__double_as_longlong(gmax0));
-        if (hasq) atomicMax(ps + 1, (unsigned long long)__double_as_longlong(gmax1));
+        gred[2 * f] = gmax0;
+        gred[2 * f + 1] = gmax1;
       }
     }
     fence_proxy_async();  // order these stores before the next block's TMA refill of buf
     __syncthreads();
+    if (pscale && threadIdx.x == 0) {  // one atomic per phase per block
+      double m0 = 0.0, m1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < W::WARPS; ++k) {
+        m0 = fmax(m0, gred[2 * k]);
+        m1 = fmax(m1, gred[2 * k + 1]);
+      }
+      unsigned long long* ps = reinterpret_cast<unsigned long long*>(pscale + p0 + pa);
+      atomicMax(ps, (unsigned long long)__double_as_longlong(m0));
+      if (hasq) atomicMax(ps + 1, (unsigned long long)__double_as_longlong(m1));
+    }
     const bool active = tl < ncol;
 #define PSWE_A_GATHER(v, sub)                                                         \
   band_gather<NX>(v, t, buf + (size_t)(fi + 3 * (sub)) * fs + (size_t)tl * Kx, active);  \

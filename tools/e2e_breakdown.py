@@ -28,3 +28,18 @@ for _ in range(n):
 torch.cuda.synchronize()
 tot = (time.perf_counter() - t0) / n
 print({k: round(1e3 * v / n, 3) for k, v in T.items()}, "full call", round(1e3 * tot, 3))
+
+# device-side: the gated full-layout call vs pack + compact + unpack (no gate)
+ctx = dynamics.context(c.state, c.params)
+U = dynamics.upload(ctx, c.state)
+def dev(fn, k=5):
+    fn(); torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(k):
+        fn()
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / k
+gated = dev(lambda: ctx.averaged_tendency(U))
+plain = dev(lambda: ctx.unpack(ctx.averaged_tendency_compact(ctx.pack(U))))
+print(f"device ms: gated full-layout {gated:.3f}  pack+compact+unpack {plain:.3f}")
