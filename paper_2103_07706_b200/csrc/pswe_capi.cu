@@ -21,6 +21,7 @@
 #include "herm_kernels.cuh"
 #include "fused_kernels.cuh"
 #include "generic_kernels.cuh"
+#include "cluster_kernels.cuh"
 
 using namespace pswe;
 
@@ -669,6 +670,62 @@ int launch_fused(pswe_ctx* c, const PhaseDev& ph, int Gc, const double2* Uc, dou
   return PSWE_OK;
 }
 
+// 64^2: one 4-CTA cluster per phase group (cluster_kernels.cuh)
+constexpr int CF_N = 64, CF_C = 4;
+
+template <bool MW>
+int launch_cfused(pswe_ctx* c, const PhaseDev& ph, int Gc, const double2* Uc, double2* out, double* pscale,
+                  cudaStream_t st) {
+  using W = CFusedW<CF_N, CF_C>;
+  auto kern = cfused_kernel<CF_N, CF_C, MW>;
+  CU(smem_attr(kern, W::bytes(), c->device));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(Gc * CF_C);
+  cfg.blockDim = dim3(W::NT);
+  cfg.dynamicSmemBytes = W::bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CF_C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->pdl ? 2 : 1;
+  ProfScope ps(c, 0, st);
+  CU(cudaLaunchKernelEx(&cfg, kern, c->grid(), c->prop(), ph, Gc, Uc, (const double2*)c->ctab_cur, out, pscale));
+  c->launches++;
+  c->variant[PSWE_V_FUSED]++;
+  CU(cudaGetLastError());
+  return PSWE_OK;
+}
+
+// clusters resident at once (one CTA per SM; clusters stay inside a GPC)
+int cfused_capacity(pswe_ctx* c) {
+  static int cached = -1;
+  if (cached > 0) return cached;
+  using W = CFusedW<CF_N, CF_C>;
+  smem_attr(cfused_kernel<CF_N, CF_C, false>, W::bytes(), c->device);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CF_C * c->sms);
+  cfg.blockDim = dim3(W::NT);
+  cfg.dynamicSmemBytes = W::bytes();
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CF_C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, cfused_kernel<CF_N, CF_C, false>, &cfg) != cudaSuccess || n < 1)
+    n = c->sms / CF_C;
+  cached = n;
+  if (getenv("PSWE_VERBOSE")) fprintf(stderr, "pswe: 64^2 cluster kernel: %d clusters resident\n", n);
+  return n;
+}
+
 template <int N>
 int fused_capacity(const pswe_ctx* c) {
   smem_attr(fused_kernel<N, false>, FusedW<N>::bytes(), c->device);  // before the occupancy query
@@ -679,10 +736,21 @@ int fused_capacity(const pswe_ctx* c) {
 // everywhere (32^2, M = 8: 30 -> 20 us; M = 256: 131 -> 63 us); at 64^2 the
 // single CTA's 8 warps are latency-bound (M = 256: 113 -> 128 us), so 64^2
 // keeps the three-pass pipeline unless PSWE_FUSED64 is set.
-bool fused_ok(const pswe_ctx* c) {
+bool cluster_ok(pswe_ctx* c, int P);
+bool fused_ok(pswe_ctx* c, int P) {
   static const bool off = getenv("PSWE_NO_FUSED") != nullptr;  // A/B switch
-  static const bool f64 = getenv("PSWE_FUSED64") != nullptr;
-  return !off && !c->gen && c->nx == c->ny && (c->nx <= 32 || (f64 && c->nx == 64));
+  static const bool single64 = getenv("PSWE_FUSED64") != nullptr;
+  return !off && !c->gen && c->nx == c->ny && (c->nx <= 32 || (c->nx == 64 && (single64 || cluster_ok(c, P))));
+}
+// 64^2: the cluster kernel while every cluster gets at most two phases
+// (tools/c64_check.py, L2 flushed: M = 8 26.2 -> 24.8 us, M = 16 32.6 ->
+// 27.7, M = 32 44.5 -> 39.9; with more phases the three passes' throughput
+// wins, M = 256 113 vs 197 us; one phase: the three passes, 23.0 vs 24.8);
+// PSWE_FUSED64: the single-CTA kernel instead (experiments)
+int cfused_capacity(pswe_ctx* c);
+bool cluster_ok(pswe_ctx* c, int P) {
+  static const bool single = getenv("PSWE_FUSED64") != nullptr;
+  return c->nx == 64 && !single && P >= 2 && P <= 2 * cfused_capacity(c);
 }
 
 // `gate`: the input was packed with the gate's statistics (pack_kernel
@@ -694,7 +762,7 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
                 bool gate = false) {
   const double* s = ps.s;
   const int P = ps.P;
-  const bool fused = fused_ok(c);
+  const bool fused = fused_ok(c, P);
   // exact route: phase table (built once per quadrature / grid)
   c->ctab_cur = nullptr;
   if (c->kind == 0) {
@@ -712,11 +780,12 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
   if (fused) {
     // one CTA per phase group, every resident CTA busy at most once
     int cap = 1;
+    const bool clu = c->nx == 64 && cluster_ok(c, P);
     switch (c->nx) {
       case 8: cap = fused_capacity<8>(c); break;
       case 16: cap = fused_capacity<16>(c); break;
       case 32: cap = fused_capacity<32>(c); break;
-      default: cap = fused_capacity<64>(c); break;
+      default: cap = clu ? cfused_capacity(c) : fused_capacity<64>(c); break;
     }
     const int Gc = std::max(1, std::min(P, cap));
     const size_t cw = (size_t)ps.W * c->compact_elems();
@@ -738,8 +807,14 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
                            : launch_fused<16, false>(c, ph, Gc, Uc, out, pscale, st); break;
       case 32: rc = ps.win ? launch_fused<32, true>(c, ph, Gc, Uc, out, pscale, st)
                            : launch_fused<32, false>(c, ph, Gc, Uc, out, pscale, st); break;
-      default: rc = ps.win ? launch_fused<64, true>(c, ph, Gc, Uc, out, pscale, st)
-                           : launch_fused<64, false>(c, ph, Gc, Uc, out, pscale, st); break;
+      default:
+        if (clu)
+          rc = ps.win ? launch_cfused<true>(c, ph, Gc, Uc, out, pscale, st)
+                      : launch_cfused<false>(c, ph, Gc, Uc, out, pscale, st);
+        else
+          rc = ps.win ? launch_fused<64, true>(c, ph, Gc, Uc, out, pscale, st)
+                      : launch_fused<64, false>(c, ph, Gc, Uc, out, pscale, st);
+        break;
     }
     TRY(rc);
     if (!direct) {

@@ -476,7 +476,7 @@ def test_chebyshev_route_step_and_run_match_oracle():
 def test_latency_paths_are_bitwise_identical(tmp_path):
     """The latency-bound paths (split pass B, programmatic dependent launch)
     change scheduling only: a run with both switched off (fresh process, the
-    switches are read once) gives the same bits for a C2 RHS and step, and
+    switches are read once) gives the same bits for a 128^2 (M = 4) RHS and step, and
     for a single-node 512^2 nonlinearity (split pass B at NY = 512).  The
     baseline run must really have taken the split path (variant counts)."""
     import os
@@ -489,9 +489,9 @@ def test_latency_paths_are_bitwise_identical(tmp_path):
         "import sys, json, numpy as np; sys.path.insert(0, %r)\n"
         "import paper_2103_07706_b200 as pk\n"
         "from paper_2103_07706_b200 import cases\n"
-        "c = cases.case_c2()\n"
+        "c = cases.case_c5(5, 4)\n"
         "a = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())\n"
-        "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
+        "cfg = pk.StepConfig(dt=600.0, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
         "s = pk.step_averaged_ssprk3(c.state, cfg, c.params)\n"
         "v = pk.dynamics.context(c.state, c.params).variant_launches\n"
         "d = cases.case_c5(7, 8)\n"
@@ -554,7 +554,7 @@ def test_poisoned_scratch_gives_the_same_bits(tmp_path):
         "import paper_2103_07706_b200 as pk\n"
         "from paper_2103_07706_b200 import cases\n"
         "outs, var = [], {}\n"
-        "for r, M in ((3, 256), (4, 8), (5, 32), (6, 128), (7, 8), (7, 64)):\n"
+        "for r, M in ((3, 256), (4, 8), (5, 4), (5, 32), (6, 128), (7, 8), (7, 64)):\n"
         "    c = cases.case_c5(r, M)\n"
         "    ctx = pk.dynamics.context(c.state, c.params)\n"
         "    ctx.set_propagator('exact')\n"
@@ -597,10 +597,11 @@ def test_poisoned_scratch_gives_the_same_bits(tmp_path):
 
 
 def test_fused_small_grid_kernel_matches_three_pass_path(tmp_path):
-    """n <= 64: the one-CTA-per-phase-group kernel (fused_kernels.cuh) vs the
-    three-pass pipeline (PSWE_NO_FUSED) -- same transforms and formulas, so
-    equal to round-off -- and vs the oracle, at every small size, one and
-    many phases per CTA, a window batch and the stepper."""
+    """n <= 64: the one-CTA-per-phase-group kernel (fused_kernels.cuh, n <= 32)
+    and the 4-CTA cluster kernel (cluster_kernels.cuh, 64^2, few phases) vs
+    the three-pass pipeline (PSWE_NO_FUSED) -- same transforms and formulas,
+    so equal to round-off -- and vs the oracle, at every small size, one and
+    many phases per CTA, a window batch and the stepper (C1, C2)."""
     import json
     import os
     import subprocess
@@ -613,14 +614,14 @@ def test_fused_small_grid_kernel_matches_three_pass_path(tmp_path):
         "import paper_2103_07706_b200 as pk\n"
         "from paper_2103_07706_b200 import cases\n"
         "outs = []\n"
-        "for r, M in ((1, 4), (2, 8), (3, 8), (3, 64), (3, 256)):\n"
+        "for r, M in ((1, 4), (2, 8), (3, 8), (3, 64), (3, 256), (4, 8), (4, 16)):\n"
         "    c = cases.case_c5(r, M)\n"
         "    a = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())\n"
         "    outs.append(np.stack([a.u, a.v, a.eta]))\n"
-        "c = cases.case_c1()\n"
-        "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
-        "s = pk.run(c.state, cfg, c.params, t_end=3 * c.dt).states[-1]\n"
-        "outs.append(np.stack([s.u, s.v, s.eta]))\n"
+        "for c in (cases.case_c1(), cases.case_c2()):\n"
+        "    cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
+        "    s = pk.run(c.state, cfg, c.params, t_end=3 * c.dt).states[-1]\n"
+        "    outs.append(np.stack([s.u, s.v, s.eta]))\n"
         "res = pk.window_sweep(c.state, c.params, c.dt, 2 * c.dt, [0.0, 1800.0, 3600.0], M=8)\n"
         "outs += [np.stack([r.final.u, r.final.v, r.final.eta]) for r in res]\n"
         "np.savez(sys.argv[1], *outs)\n"
