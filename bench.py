@@ -410,6 +410,7 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     case = cases.case_c5(args.level, args.M)
     n, P = case.grid.nx, case.P
+    free0 = torch.cuda.mem_get_info(dev)[0]
     ctx = pk.dynamics.context(case.state, case.params)
     ctx.set_propagator("exact")
     ctx.set_quadrature(case.quadrature.s, case.quadrature.w)
@@ -421,9 +422,29 @@ def run_ours(args, ws, rank, local):
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
+    # setup outside the timed region, stated: the first evaluation also builds
+    # the quadrature's (c1, c2) phase table (once per quadrature, as the
+    # reference builds its quadrature once per window) and allocates scratch
+    def timed_eval():
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.averaged_tendency_compact(Uc, Ac)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+    first_ms = timed_eval()
     for _ in range(args.warmup):
         ctx.averaged_tendency_compact(Uc, Ac)
     torch.cuda.synchronize()
+    steady_ms = timed_eval()
+    Kx, Ky = 2 * (n // 3) + 1, n // 3 + 1
+    setup = {"first_call_ms": first_ms, "steady_call_ms": steady_ms,
+             "phase_table_build_ms_approx": max(0.0, first_ms - steady_ms),
+             "phase_table_bytes": P * Ky * Kx * 16,
+             "device_memory_bytes": free0 - torch.cuda.mem_get_info(dev)[0] - flush.numel() * 4,
+             "note": "outside the timed region: the (c1, c2) phase table (once per quadrature) and the "
+                     "context's scratch (chunk intermediates, slots); device_memory_bytes = the context's "
+                     "footprint incl. inputs/outputs"}
 
     # ---- timed region: device time of K evaluations, L2 flushed before each
     sampler = ClockSampler(local)
@@ -548,6 +569,7 @@ def run_ours(args, ws, rank, local):
             "roofline": roofline, "rhs_roofline": rhs_roofline, "fp64": fp64, "kernels": kern,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "gpu": torch.cuda.get_device_name(local), "sweep": sweep, "step_configs": steps_info,
+            "setup": setup,
         }
         if cpu is not None and "parity" in cpu:
             line["parity"] = cpu["parity"]
