@@ -32,6 +32,14 @@
 #include "tmem.cuh"
 #include "wfft.cuh"
 
+#ifdef PSWE_EARLY_STWAIT  // A/B switch: wait right after every tensor-memory store
+#define PSWE_ST_WAIT_EARLY() tmem_wait_st()
+#define PSWE_ST_WAIT_LATE()
+#else
+#define PSWE_ST_WAIT_EARLY()
+#define PSWE_ST_WAIT_LATE() tmem_wait_st()
+#endif
+
 namespace pswe {
 
 struct GridDev {
@@ -843,10 +851,13 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
         else if (sub + 1 < nsub) issue(sub + 1, 0);
         wfft_t1<NY, true, true>(v, t, xb, wl);
       }
+      // tensor-memory stores are waited for (tcgen05.wait::st) only before
+      // the first load of the same columns, a transform later
       if (it == 0) {
         tmem_stash16(taddr, v);
-        tmem_wait_st();
+        PSWE_ST_WAIT_EARLY();
       } else if (it == 1) {
+        PSWE_ST_WAIT_LATE();  // (u, v) of it == 0
 #pragma unroll
         for (int i0 = 0; i0 < P; i0 += 4) {
           double2 q[4];
@@ -855,8 +866,9 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
           for (int k = 0; k < 4; ++k) pa_[i0 + k] = -(q[k].x * v[i0 + k].x + q[k].y * v[i0 + k].y);
         }
         tmem_stash16d(taddr + 64, pa_);
-        tmem_wait_st();
+        PSWE_ST_WAIT_EARLY();
       } else if (it == 2) {
+        PSWE_ST_WAIT_LATE();  // A of it == 1
 #pragma unroll
         for (int i0 = 0; i0 < P; i0 += 4) {
           double2 q[4];
@@ -876,9 +888,10 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
 #pragma unroll
             for (int i = 0; i < P; ++i) dd[i] = v[i].y;
             tmem_stash16d(taddr + 96, dd);
-            tmem_wait_st();
+            PSWE_ST_WAIT_EARLY();
           }
         } else {
+          PSWE_ST_WAIT_LATE();  // d_p1 of sub 0
 #pragma unroll
           for (int i0 = 0; i0 < P; i0 += 4) {
             uint32_t r[8];
