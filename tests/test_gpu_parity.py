@@ -648,3 +648,30 @@ def test_fused_small_grid_kernel_matches_three_pass_path(tmp_path):
                                  for sc in (1.0, 1.0, 50.0)])
     got = pk.averaged_tendency(state_from(U, g), c.quadrature, c.params, pk.PropagatorSpec.exact())
     assert O.rel_l2(arr(got), O.averaged_tendency(S, U, c.quadrature.s, c.quadrature.w, workers=8)) <= RHS_TOL
+
+
+def test_generic_sizes_chebyshev_window_batch_and_gate():
+    """The generic kernels (48^2 = 3 * 2^4) under the other routes: the
+    Chebyshev exponential vs the oracle, a two-window batch vs one-by-one
+    runs, and a non-Hermitian input failing with the reference's message."""
+    n = 48
+    rng = np.random.default_rng(48)
+    g = pk.make_grid(n, n, 4.0e7, 4.0e7)
+    S = O.Setup(n, n, g.Lx, g.Ly, F0, G0, H0)
+    U = np.stack([O.truncate(O.spectral(sc * rng.standard_normal((n, n))), S.mask) for sc in (1.0, 1.0, 50.0)])
+    p = flat(g)
+    st = state_from(U, g)
+    lam = pk.max_frequency(g, p)
+    spec = pk.PropagatorSpec.chebyshev(lam * 3600.0)
+    q = pk.kernel_weights(1800.0, 4)
+    got = pk.averaged_tendency(st, q, p, spec)
+    want = O.averaged_tendency(S, U, q.s, q.w, O.Propagator("chebyshev", spec.Lambda, spec.n_poly))
+    assert O.rel_l2(arr(got), want) <= RHS_TOL
+    res = pk.window_sweep(st, p, 900.0, 1800.0, [0.0, 1800.0], M=4)
+    for r in res:
+        solo = pk.run(st, pk.make_step_config(g, p, dt=900.0, T=r.T, M=4 if r.T > 0 else 0), p, 1800.0)
+        assert rel_l2(arr(r.final), arr(solo.states[-1])) <= 1e-13
+    bad = U.copy()
+    bad[0, 3, 5] += 1e-6 * np.max(np.abs(U[0]))
+    with pytest.raises(RuntimeError, match=r"averaging node k = -3 .*non-Hermitian spectral field: mode"):
+        pk.averaged_tendency(state_from(bad, g), q, p, pk.PropagatorSpec.exact())
