@@ -837,10 +837,12 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
   // multiple of `lanes` equal chunks no larger than chunk_bytes, so the lanes
   // finish together.
   const int cpmax = (int)std::max<size_t>(1, c->chunk_bytes / (per_phase * sizeof(double2)));
-  // at least one chunk per lane when a chunk still holds >= 16 phases and
+  // at least one chunk per lane when a chunk still holds >= 8 phases and
   // >= 24 MiB of intermediates: the lanes' overlap is then worth more than
-  // the larger per-launch grids of fewer chunks
-  static const int minph_floor = getenv("PSWE_MINPH") ? atoi(getenv("PSWE_MINPH")) : 16;  // tuning experiments
+  // the larger per-launch grids of fewer chunks (tools/lane_sweep.sh: 8
+  // instead of 16 phases gains 1.6-1.7 % at 256^2 / 512^2, M = 32; other
+  // points unchanged)
+  static const int minph_floor = getenv("PSWE_MINPH") ? atoi(getenv("PSWE_MINPH")) : 8;  // tuning experiments
   static const int minmb = getenv("PSWE_MINMB") ? atoi(getenv("PSWE_MINMB")) : 24;
   const int minph = std::max<int>(minph_floor, (int)(((size_t)minmb << 20) / (per_phase * sizeof(double2))));
   int nchunks = std::max((P + cpmax - 1) / cpmax, std::min(c->n_lanes, P / minph));

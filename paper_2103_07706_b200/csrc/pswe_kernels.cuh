@@ -1106,14 +1106,25 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   }
 }
 
-// ordered sum of the phase-group slots -> compact tendency
+// ordered sum of the phase-group slots -> compact tendency.  The loads of a
+// batch of slots are issued before the (fixed-order) additions: a serial
+// load-add chain over Gc slots was latency-bound at small sizes (64^2, M = 8:
+// ~6 us for 0.7 MB).
 __global__ void reduce_slots_kernel(const double2* __restrict__ slots, int Gc, size_t n,
                                     double2* __restrict__ out) {
   griddep_wait();
   griddep_launch();
+  constexpr int B = 8;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     double2 a = slots[i];
-    for (int g = 1; g < Gc; ++g) a = cadd(a, slots[(size_t)g * n + i]);
+    for (int g0 = 1; g0 < Gc; g0 += B) {
+      double2 v[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k) v[k] = g0 + k < Gc ? slots[(size_t)(g0 + k) * n + i] : czero();
+#pragma unroll
+      for (int k = 0; k < B; ++k)
+        if (g0 + k < Gc) a = cadd(a, v[k]);
+    }
     out[i] = a;
   }
 }
