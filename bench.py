@@ -530,16 +530,26 @@ def run_ours(args, ws, rank, local):
             out = pk.averaged_tendency(case.state, quad, case.params, spec)
         torch.cuda.synchronize()
         barrier(ws)
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            out = pk.averaged_tendency(case.state, quad, case.params, spec)
-        torch.cuda.synchronize()
-        e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
+        # three contiguous blocks of calls; the block with the median time
+        # stands (a host-side stall of the box -- seen up to +0.6 ms per call
+        # on some boxes -- does not decide the figure; every block is an
+        # honest back-to-back throughput)
+        blocks = []
+        per = max(1, args.e2e_steps // 3)
+        for _ in range(3):
+            t0 = time.perf_counter()
+            for _ in range(per):
+                out = pk.averaged_tendency(case.state, quad, case.params, spec)
+            torch.cuda.synchronize()
+            blocks.append(time.perf_counter() - t0)
+        e2e_s = max_over_ranks(sorted(blocks)[1] * args.e2e_steps / per, ws, dev)
         e2e = {"value": ws * P * case.dof * args.e2e_steps / e2e_s, "unit": UNIT,
                # the drop-in call moves only the fields' 2/3 band (pswe_copy_band)
                "h2d_bytes_per_step": 3 * band_bytes(n, n), "d2h_bytes_per_step": 3 * band_bytes(n, n),
                "ms_per_step": 1e3 * e2e_s / args.e2e_steps,
-               "path": "paper_2103_07706_b200.averaged_tendency(numpy State) -> C ABI -> numpy State"}
+               "path": "paper_2103_07706_b200.averaged_tendency(numpy State) -> C ABI -> numpy State",
+               "timing": f"median of 3 blocks of {max(1, args.e2e_steps // 3)} back-to-back calls",
+               "block_ms_per_call": [1e3 * b / max(1, args.e2e_steps // 3) for b in blocks]}
         del out
 
     sweep = None
