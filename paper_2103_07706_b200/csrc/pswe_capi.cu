@@ -703,8 +703,9 @@ int launch_cfused(pswe_ctx* c, const PhaseDev& ph, int Gc, const double2* Uc, do
 
 // clusters resident at once (one CTA per SM; clusters stay inside a GPC)
 int cfused_capacity(pswe_ctx* c) {
-  static int cached = -1;
-  if (cached > 0) return cached;
+  static std::atomic<int> cached[64];  // per device ordinal (0 = not yet queried)
+  const int dev = c->device & 63;
+  if (cached[dev].load() > 0) return cached[dev].load();
   using W = CFusedW<CF_N, CF_C>;
   smem_attr(cfused_kernel<CF_N, CF_C, false>, W::bytes(), c->device);
   cudaLaunchConfig_t cfg = {};
@@ -721,7 +722,7 @@ int cfused_capacity(pswe_ctx* c) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, cfused_kernel<CF_N, CF_C, false>, &cfg) != cudaSuccess || n < 1)
     n = c->sms / CF_C;
-  cached = n;
+  cached[dev].store(n);
   if (getenv("PSWE_VERBOSE")) fprintf(stderr, "pswe: 64^2 cluster kernel: %d clusters resident\n", n);
   return n;
 }
