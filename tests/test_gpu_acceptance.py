@@ -99,6 +99,29 @@ def test_averaging_window_has_interior_optimum_and_is_deterministic():
     assert ctx.launch_count > 0
 
 
+def test_window_sweep_matches_the_reference_run():
+    """The same 15-day experiment against the unmodified reference's own
+    result (tests/golden/acceptance_sweep.npz, written by
+    oracle/make_acceptance_golden.py from phaseswe: 360 averaged steps per
+    window and the 7200-step reference): final states to the north_star
+    run tolerance (rel L2 <= 1e-8) and the normalized errors."""
+    from conftest import load_golden, rel_l2
+    z = load_golden("acceptance_sweep")
+    g, rough, jet = default_problem()
+    t_end = 15 * 86400.0
+    ref = pk.run(jet, pk.make_step_config(g, rough, dt=180.0, T=0.0), rough, t_end).states[-1]
+    assert rel_l2(np.stack([ref.u, ref.v, ref.eta]), z["reference"]) <= 1e-8
+    res = pk.window_sweep(jet, rough, 3600.0, t_end, list(z["T"]), reference=ref)
+    for k, r in enumerate(res):
+        assert r.M == int(z["M"][k])
+        err = rel_l2(np.stack([r.final.u, r.final.v, r.final.eta]), z["finals"][k])
+        print(f"T = {r.T:g} s: final state rel L2 vs the reference {err:.2e}; "
+              f"l2_eta {r.l2_eta:.6g} (reference {z['l2_eta'][k]:.6g})")
+        assert err <= 1e-8
+        assert abs(r.l2_eta - z["l2_eta"][k]) <= 1e-6 * z["l2_eta"][k]
+        assert abs(r.l2_u - z["l2_u"][k]) <= 1e-6 * z["l2_u"][k]
+
+
 def truncated_convolution(grid, ca, cb):
     """Direct O(n^4) truncated-convolution sum (the reference's conftest.py oracle, restated)."""
     nx, ny = grid.nx, grid.ny
