@@ -27,8 +27,10 @@ struct FftPlan {
   const double2* tw;  // W_n^k = e^{-2 pi i k / n}, k = 0..n-1
 };
 
+// W_n^e for 0 <= e < n (every caller's exponent is already reduced: the
+// stage twiddle r k n / (Ns R) < n, the DFT_R twiddle ((q r) mod R) n / R < n)
 __device__ __forceinline__ double2 twp(const FftPlan& pl, long long e, bool inv) {
-  double2 w = __ldg(pl.tw + (int)(e % pl.n));
+  double2 w = __ldg(pl.tw + (int)e);
   if (inv) w.y = -w.y;
   return w;
 }

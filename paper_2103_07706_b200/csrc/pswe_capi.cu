@@ -619,6 +619,14 @@ int gen_groups(const pswe_ctx* c, int CP) {
   return std::max(1, std::min(want, std::max(1, CP / 2)));
 }
 
+// threads per generic CTA: about one per radix-4 butterfly of its transform
+// length (a whole CTA of 256 threads on a 96-point transform left most of
+// them idle), whole warps, at most GEN_THREADS
+int gen_threads(int n, int modes = 0) {
+  const int want = std::max(n / 4, modes / 2);
+  return std::min(GEN_THREADS, std::max(32, (want + 31) / 32 * 32));
+}
+
 int launch_gen(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int first, const double2* Uc, double2* I1,
                double2* I2, double2* slots, double* pscale, cudaStream_t st) {
   const size_t sA = ((size_t)3 * c->Kx + 2 * (size_t)c->nx) * sizeof(double2);
@@ -630,21 +638,21 @@ int launch_gen(pswe_ctx* c, const PhaseDev& ph, int p0, int np, int Gc, int firs
   CU(smem_attr(gen_passC_kernel<true>, sC, c->device));
   {
     ProfScope ps(c, 0, st);
-    CU(launch_k(c->pdl, gen_passA_kernel, np * c->Ky, GEN_THREADS, sA, st, c->grid(), c->prop(), ph, p0, np, Uc,
+    CU(launch_k(c->pdl, gen_passA_kernel, np * c->Ky, gen_threads(c->nx, c->Kx), sA, st, c->grid(), c->prop(), ph, p0, np, Uc,
                 c->ctab_cur, I1, c->plx, pscale));
   }
   {
     ProfScope ps(c, 1, st);
-    CU(launch_k(c->pdl, gen_passB_kernel, np * c->nx, GEN_THREADS, sB, st, c->grid(), np, (const double2*)I1, I2,
+    CU(launch_k(c->pdl, gen_passB_kernel, np * c->nx, gen_threads(c->ny), sB, st, c->grid(), np, (const double2*)I1, I2,
                 c->ply));
   }
   {
     ProfScope ps(c, 2, st);
     if (ph.win)
-      CU(launch_k(c->pdl, gen_passC_kernel<true>, c->Ky * Gc, GEN_THREADS, sC, st, c->grid(), c->prop(), ph, p0, np,
+      CU(launch_k(c->pdl, gen_passC_kernel<true>, c->Ky * Gc, gen_threads(c->nx, c->Kx), sC, st, c->grid(), c->prop(), ph, p0, np,
                   Gc, (const double2*)I2, c->ctab_cur, slots, first, c->plx));
     else
-      CU(launch_k(c->pdl, gen_passC_kernel<false>, c->Ky * Gc, GEN_THREADS, sC, st, c->grid(), c->prop(), ph, p0,
+      CU(launch_k(c->pdl, gen_passC_kernel<false>, c->Ky * Gc, gen_threads(c->nx, c->Kx), sC, st, c->grid(), c->prop(), ph, p0,
                   np, Gc, (const double2*)I2, c->ctab_cur, slots, first, c->plx));
   }
   c->launches += 3;
@@ -1829,9 +1837,9 @@ static int physical_fields(pswe_ctx* c, const double* u, const double* v, const 
     const size_t sc = (size_t)2 * c->nx * sizeof(double2), sr = (size_t)4 * c->ny * sizeof(double2);
     CU(smem_attr(gen_diag_cols_kernel, sc, c->device));
     CU(smem_attr(gen_diag_rows_kernel, sr, c->device));
-    gen_diag_cols_kernel<<<4 * (c->ny / 2 + 1), GEN_THREADS, sc, st>>>(c->grid(), U, V, E, c->bfull.p,
+    gen_diag_cols_kernel<<<4 * (c->ny / 2 + 1), gen_threads(c->nx), sc, st>>>(c->grid(), U, V, E, c->bfull.p,
                                                                         c->diag_cols.p, c->plx);
-    gen_diag_rows_kernel<<<c->nx, GEN_THREADS, sr, st>>>(c->grid(), c->diag_cols.p, c->H, c->g, c->diag_part.p,
+    gen_diag_rows_kernel<<<c->nx, gen_threads(c->ny), sr, st>>>(c->grid(), c->diag_cols.p, c->H, c->g, c->diag_part.p,
                                                           phys, c->ply);
     c->launches += 2;
     CU(cudaGetLastError());
