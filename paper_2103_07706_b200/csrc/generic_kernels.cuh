@@ -7,8 +7,8 @@
 // Same data layouts and the same pass structure as pswe_kernels.cuh (the
 // host orchestration -- chunks, lanes, slots, ordered reduction, gate -- is
 // shared), but every transform is one CTA-cooperative mixed-radix Stockham
-// FFT in shared memory: radices 4, 2, 3, 5, 7 and a direct DFT for any other
-// prime factor, twiddles read from the exact W_n^k table (twiddle_kernel).
+// FFT in shared memory: radices 16, 8, 4, 2 as register DFTs, a direct DFT
+// for the odd prime factors, twiddles read from the exact W_n^k table (twiddle_kernel).
 // These kernels trade speed for generality; the power-of-two sizes keep the
 // tuned kernels.
 #pragma once
@@ -35,6 +35,32 @@ __device__ __forceinline__ double2 twp(const FftPlan& pl, long long e, bool inv)
   return w;
 }
 
+// One Stockham butterfly of compile-time radix R (register DFT): inputs
+// x[j + r m] twiddled by W^{r k n / (Ns R)}, outputs y[base + q Ns].
+template <int R, bool INV>
+__device__ __forceinline__ void gen_bfly(const double2* x, double2* y, const FftPlan& pl, int j, int m, int Ns) {
+  const int n = pl.n, k = j % Ns;
+  double2 v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double2 z = x[j + r * m];
+    if (r) z = cmul(z, twp(pl, (long long)r * k * (n / (Ns * R)), INV));
+    v[r] = z;
+  }
+  if constexpr (R == 2) {
+    dft2<INV>(v[0], v[1]);
+  } else if constexpr (R == 4) {
+    dft4<INV>(v[0], v[1], v[2], v[3]);
+  } else if constexpr (R == 8) {
+    dft8<INV>(v);
+  } else {
+    dft16<INV>(v);
+  }
+  const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+  for (int q = 0; q < R; ++q) y[base + q * Ns] = v[q];
+}
+
 // CTA-cooperative Stockham FFT of `a` (length pl.n, shared memory) with
 // scratch `b`; the result ends in the returned buffer (a or b).  All
 // threads of the CTA must call it.  INV: unnormalised e^{+...}.
@@ -47,43 +73,23 @@ __device__ double2* gen_fft(double2* a, double2* b, const FftPlan& pl) {
     const int R = pl.f[s];
     const int m = n / R;
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
-      const int k = j % Ns;
-      double2 v[8];
-      if (R <= 8) {
-        for (int r = 0; r < R; ++r) {
-          double2 z = x[j + r * m];
-          if (r) z = cmul(z, twp(pl, (long long)r * k * (n / (Ns * R)), INV));
-          v[r] = z;
-        }
-        const int base = (j / Ns) * Ns * R + k;
-        if (R == 2) {
-          y[base] = cadd(v[0], v[1]);
-          y[base + Ns] = csub(v[0], v[1]);
-        } else if (R == 4) {
-          double2 y0 = v[0], y1 = v[1], y2 = v[2], y3 = v[3];
-          dft4<INV>(y0, y1, y2, y3);
-          y[base] = y0;
-          y[base + Ns] = y1;
-          y[base + 2 * Ns] = y2;
-          y[base + 3 * Ns] = y3;
-        } else {
-          for (int q = 0; q < R; ++q) {  // direct DFT_R with table twiddles W_R^{qr} = W_n^{qr n/R}
-            double2 acc = v[0];
-            for (int r = 1; r < R; ++r) acc = cfma(twp(pl, (long long)((q * r) % R) * (n / R), INV), v[r], acc);
+      switch (R) {
+        case 16: gen_bfly<16, INV>(x, y, pl, j, m, Ns); break;
+        case 8: gen_bfly<8, INV>(x, y, pl, j, m, Ns); break;
+        case 4: gen_bfly<4, INV>(x, y, pl, j, m, Ns); break;
+        case 2: gen_bfly<2, INV>(x, y, pl, j, m, Ns); break;
+        default: {
+          // odd prime radix: direct DFT_R with table twiddles W_R^{qr} = W_n^{qr n/R}
+          const int k = j % Ns, base = (j / Ns) * Ns * R + k;
+          for (int q = 0; q < R; ++q) {
+            double2 acc = czero();
+            for (int r = 0; r < R; ++r) {
+              double2 z = x[j + r * m];
+              if (r) z = cmul(z, twp(pl, (long long)r * k * (n / (Ns * R)), INV));
+              acc = r ? cfma(twp(pl, (long long)((q * r) % R) * (n / R), INV), z, acc) : z;
+            }
             y[base + q * Ns] = acc;
           }
-        }
-      } else {
-        // a large prime factor: direct DFT reading the inputs on the fly
-        const int base = (j / Ns) * Ns * R + k;
-        for (int q = 0; q < R; ++q) {
-          double2 acc = czero();
-          for (int r = 0; r < R; ++r) {
-            double2 z = x[j + r * m];
-            if (r) z = cmul(z, twp(pl, (long long)r * k * (n / (Ns * R)), INV));
-            acc = cadd(acc, cmul(twp(pl, (long long)((q * r) % R) * (n / R), INV), z));
-          }
-          y[base + q * Ns] = acc;
         }
       }
     }

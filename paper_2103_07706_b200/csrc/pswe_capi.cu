@@ -605,7 +605,9 @@ FftPlan make_plan(int n, const double2* tw) {
   p.n = n;
   p.tw = tw;
   int m = n;
-  while (m % 4 == 0 && p.nf < GEN_MAX_FACTORS) { p.f[p.nf++] = 4; m /= 4; }
+  // large register radices first: fewer shared-memory passes and barriers
+  for (int r : {16, 8, 4})
+    while (m % r == 0 && p.nf < GEN_MAX_FACTORS) { p.f[p.nf++] = r; m /= r; }
   for (int r : {2, 3, 5, 7})
     while (m % r == 0 && p.nf < GEN_MAX_FACTORS) { p.f[p.nf++] = r; m /= r; }
   for (int r = 11; m > 1 && p.nf < GEN_MAX_FACTORS; r += 2)
@@ -623,7 +625,7 @@ int gen_groups(const pswe_ctx* c, int CP) {
 // length (a whole CTA of 256 threads on a 96-point transform left most of
 // them idle), whole warps, at most GEN_THREADS
 int gen_threads(int n, int modes = 0) {
-  const int want = std::max(n / 4, modes / 2);
+  const int want = std::max(n / 8, modes / 2);
   return std::min(GEN_THREADS, std::max(32, (want + 31) / 32 * 32));
 }
 
