@@ -846,9 +846,13 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
         else
           build_pair_t<NY, false, false>(v, t, mypre, kys);
         __syncwarp();  // prefetch buffer consumed
-        // queue the next transform's inputs
-        if (it < 3) issue(sub, it + 1);
-        else if (sub + 1 < nsub) issue(sub + 1, 0);
+        // queue the next input transform: (0,0) (0,1) (0,2) (0,3) [(1,0) (1,1) (1,2)];
+        // nothing after the last ((1,3) reuses the shared depth transform of (0,3))
+        const bool last = nsub == 2 ? (sub == 1 && it == 2) : it == 3;
+        if (!last) {
+          if (it < 3) issue(sub, it + 1);
+          else issue(sub + 1, 0);
+        }
         wfft_t1<NY, true, true>(v, t, xb, wl);
       }
       // tensor-memory stores are waited for (tcgen05.wait::st) only before
