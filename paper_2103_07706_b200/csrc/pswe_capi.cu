@@ -122,6 +122,10 @@ struct pswe_ctx {
   cudaStream_t st_lane[MAX_LANES - 1] = {};  // chunk lanes 1.. (lane 0 is the caller's stream)
   cudaEvent_t ev_lane[MAX_LANES - 1] = {};
   int n_lanes = 4;
+  // cached TMA tensor maps of each lane's intermediates (rhs_compact)
+  CUtensorMap map_rows[MAX_LANES], map_tiles[MAX_LANES];
+  const double2* map_base[MAX_LANES] = {};
+  int map_cp[MAX_LANES] = {};
   // cached CUDA graph of one SSPRK3 step (pswe_run)
   cudaGraphExec_t step_exec = nullptr;
   double graph_dt = 0.0;
@@ -880,11 +884,18 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
   ph.W = ps.W;
   ph.ustride = c->compact_elems();
   cudaStream_t lst[pswe_ctx::MAX_LANES] = {st, c->st_lane[0], c->st_lane[1], c->st_lane[2]};
-  CUtensorMap mrow[pswe_ctx::MAX_LANES], mcol[pswe_ctx::MAX_LANES];
+  // the lanes' tensor maps, encoded again only when the intermediates or
+  // the chunk size change (the driver call costs microseconds, which the
+  // latency-bound small sizes would see as launch gaps)
+  CUtensorMap* mrow = c->map_rows;
+  CUtensorMap* mcol = c->map_tiles;
   for (int L = 0; L < lanes && !c->gen; ++L) {
     double2* I1 = c->inter.p + (size_t)L * per_phase * CP;
+    if (c->map_base[L] == I1 && c->map_cp[L] == CP) continue;
     TRY(map_rows_I1(c, I1, CP, &mrow[L]));
     TRY(map_tiles_I2(c, I1 + (size_t)5 * c->Ky * c->nx * CP, CP, &mcol[L]));
+    c->map_base[L] = I1;
+    c->map_cp[L] = CP;
   }
   if (lanes > 1) {
     CU(cudaEventRecord(c->ev_fork, st));
