@@ -570,8 +570,12 @@ int map_tiles_I2(const pswe_ctx* c, double2* I2, int CP, CUtensorMap* m) {
 // Averaged RHS on compact data: chunks of phases through passes A, B, C,
 // then the ordered slot reduction.  `P` live phases in (s, w) device arrays.
 // Hermitian gate scratch: zeroed once, kept zeroed by herm_eval_kernel
+// layout: [0..3) statistic A, [4..7) statistic B (the stepper alternates:
+// a stage kernel evaluates one while packing the next RHS's into the
+// other), [8..8+P) per-phase scales
+constexpr int HG_A = 0, HG_B = 4, HG_SCALE = 8;
 int ensure_hgate(pswe_ctx* c, int P) {
-  const size_t need = 4 + (size_t)std::max(P, 1);
+  const size_t need = HG_SCALE + (size_t)std::max(P, 1);
   if (c->hgate_n >= need) return PSWE_OK;
   TRY(c->hgate.alloc(need));
   CU(cudaMemset(c->hgate.p, 0, need * sizeof(double)));
@@ -594,8 +598,8 @@ PhaseSet quad_phases(pswe_ctx* c) {
   return {c->s_dev.p, c->w_dev.p, nullptr, (int)c->s_live.size(), 1, &c->ctab_q, &c->ctab_q_valid};
 }
 PhaseSet zero_phases(pswe_ctx* c) { return {c->zero_s.p, c->one_w.p, nullptr, 1, 1, &c->ctab_0, &c->ctab_0_valid}; }
-HermGate hgate_of(pswe_ctx* c, int P, int bit) {
-  return HermGate{c->hgate.p, c->hgate.p + 4, P, c->bdef, c->H, c->g, c->flags.p, bit};
+HermGate hgate_of(pswe_ctx* c, int P, int bit, int stat = HG_A) {
+  return HermGate{c->hgate.p + stat, c->hgate.p + HG_SCALE, P, c->bdef, c->H, c->g, c->flags.p, bit};
 }
 HermGate no_gate() { return HermGate{nullptr, nullptr, 0, 0.0, 1.0, 1.0, nullptr, -1}; }
 
@@ -813,7 +817,7 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
     ph.win = ps.win;
     ph.W = ps.W;
     ph.ustride = c->compact_elems();
-    double* pscale = gate ? c->hgate.p + 4 : nullptr;
+    double* pscale = gate ? c->hgate.p + HG_SCALE : nullptr;
     int rc = PSWE_OK;
     switch (c->nx) {
       case 8: rc = ps.win ? launch_fused<8, true>(c, ph, Gc, Uc, out, pscale, st)
@@ -912,11 +916,11 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
     // node) is the output itself: pass C writes it, no reduction launch
     double2* sl = direct ? Ac : c->slots.p + (size_t)L * Gc * cw;
     if (c->gen) {
-      TRY(launch_gen(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, Uc, I1, I2, sl, gate ? c->hgate.p + 4 : nullptr,
+      TRY(launch_gen(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, Uc, I1, I2, sl, gate ? c->hgate.p + HG_SCALE : nullptr,
                      lst[L]));
       continue;
     }
-    TRY(dispatchA(c, ph, p0, np, Uc, I1, gate ? c->hgate.p + 4 : nullptr, lst[L]));
+    TRY(dispatchA(c, ph, p0, np, Uc, I1, gate ? c->hgate.p + HG_SCALE : nullptr, lst[L]));
     TRY(dispatchB(c, np, lanes, mrow[L], mcol[L], I2, lst[L]));
     TRY(dispatchC(c, ph, p0, np, Gc, chunk < lanes ? 1 : 0, I2, sl, lst[L]));
   }
@@ -1070,34 +1074,27 @@ int step_impl_w(pswe_ctx* c, const PhaseSet& ps, double dt, Full3 U, Full3w out,
   const Prop pr = c->prop();
   TRY(ensure_hgate(c, ps.P));
   const int gb = elem_grid(c, (size_t)W * n), gp = elem_grid(c, (size_t)W * c->compact_elems());
-  // stage 1
+  // stage 1 (its input packed here; the stage kernels pack the inputs of
+  // RHS 2 and 3 themselves, alternating the gate statistic A / B)
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, U.u, U.v, U.e, Uc, c->hgate.p, W, ws));
+  CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, U.u, U.v, U.e, Uc, c->hgate.p + HG_A, W, ws));
   c->launches++;
   TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)Ac, edt, u1, c->flags.p, W, ws,
-              hgate_of(c, ps.P, HERM_BIT0)));
+              hgate_of(c, ps.P, HERM_BIT0, HG_A), PackOut{Uc, c->hgate.p + HG_B}));
   c->launches++;
   // stage 2
-  c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, (const double2*)u1.u, (const double2*)u1.v,
-              (const double2*)u1.e, Uc, c->hgate.p, W, ws));
-  c->launches++;
   TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage2_kernel, gb, 256, 0, st, G, pr, dt, U, f3c(u1), (const double2*)Ac, u2, c->flags.p, W,
-              ws, hgate_of(c, ps.P, HERM_BIT0 + 1)));
+              ws, hgate_of(c, ps.P, HERM_BIT0 + 1, HG_B), PackOut{Uc, c->hgate.p + HG_A}));
   c->launches++;
   // stage 3
-  c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, pack_kernel, gp, 256, 0, st, G, (const double2*)u2.u, (const double2*)u2.v,
-              (const double2*)u2.e, Uc, c->hgate.p, W, ws));
-  c->launches++;
   TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
   CU(launch_k(c->pdl, stage3_kernel, gb, 256, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)Ac, out,
-              c->flags.p, W, ws, hgate_of(c, ps.P, HERM_BIT0 + 2)));
+              c->flags.p, W, ws, hgate_of(c, ps.P, HERM_BIT0 + 2, HG_A)));
   c->launches++;
   CU(cudaGetLastError());
   return PSWE_OK;

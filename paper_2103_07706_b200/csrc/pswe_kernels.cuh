@@ -1267,14 +1267,60 @@ __device__ __forceinline__ void flag_nonfinite(const C3& q, int stage, int* flag
 __device__ __forceinline__ Full3 wshift(const Full3& a, size_t o) { return {a.u + o, a.v + o, a.e + o}; }
 __device__ __forceinline__ Full3w wshift(const Full3w& a, size_t o) { return {a.u + o, a.v + o, a.e + o}; }
 
+// The next RHS's packed input, written by the stage kernel that produces it
+// (the pack launch of stages 2 and 3 saved): the thread of a full mode k in
+// the packed half band also evaluates its mirror -k and writes
+// Uc[f][ky][kx] = (o(k) + conj o(-k)) / 2 plus the Hermitian gate's
+// statistic max |o(k) - conj o(-k)|^2 per field (as pack_kernel does).
+struct PackOut {
+  double2* Uc;    // W compact states, or nullptr: no packing
+  double* hstat;  // [3] the gate's statistic for that RHS
+};
+
+// compact index (j, r) of full mode (ix, jy) if it lies in the packed half band
+__device__ __forceinline__ bool packed_mode(const GridDev& G, int ix, int jy, int& j, int& r) {
+  const int wx = ix < G.nx / 2 ? ix : ix - G.nx;
+  if (jy > G.kym || abs(wx) > G.kxm) return false;
+  j = jy;
+  r = wx >= 0 ? wx : wx + G.Kx;
+  return true;
+}
+
+__device__ __forceinline__ void pack_store(const GridDev& G, const PackOut& po, size_t wo, int j, int r, const C3& o,
+                                           const C3& om, double (&dmax)[3]) {
+  const size_t KyKx = (size_t)G.Ky * G.Kx, i = wo + (size_t)j * G.Kx + r;
+  const double2 a[3] = {o.u, o.v, o.e}, b[3] = {om.u, om.v, om.e};
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    po.Uc[i + f * KyKx] = cmk(0.5 * (a[f].x + b[f].x), 0.5 * (a[f].y - b[f].y));
+    const double dx = a[f].x - b[f].x, dy = a[f].y + b[f].y;
+    dmax[f] = nanmax(fma(dx, dx, dy * dy), dmax[f]);
+  }
+}
+
+__device__ __forceinline__ void pack_stats_flush(const PackOut& po, double (&dmax)[3]) {
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    double m = dmax[f];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m != 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(po.hstat + f), (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+__device__ __forceinline__ int mirror_ix(const GridDev& G, int ix) { return (G.nx - ix) % G.nx; }
+__device__ __forceinline__ int mirror_jy(const GridDev& G, int jy) { return (G.ny - jy) % G.ny; }
+
 // stage 1 (integrator.py:96-98): e_dt = E(dt) U;  u1 = e_dt + dt * E(dt) A(U)
 __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const double2* __restrict__ Ac,
                               Full3w edt, Full3w u1, int* flags, int W, size_t ws,
-                              HermGate hg) {
+                              HermGate hg, PackOut po) {
   griddep_wait();
   griddep_launch();
   if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
   const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
+  double dmax[3] = {0.0, 0.0, 0.0};
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
     const size_t t = i0 + threadIdx.x;
     C3 o = c3zero();
@@ -1282,25 +1328,37 @@ __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const doub
       const size_t win = t / n, i = t - win * n;
       const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
       const double kx = G.kxf[ix], ky = G.kyf[jy];
-      const C3 e = expL(dt, ld3(wshift(U, win * ws), i), G.ph, kx, ky, pr);
+      const Full3 Uw = wshift(U, win * ws);
+      const C3 e = expL(dt, ld3(Uw, i), G.ph, kx, ky, pr);
       const C3 ea = expL(dt, compact_at(G, Ac + win * cs, ix, jy), G.ph, kx, ky, pr);
       o = c3add(e, c3scale(dt, ea));
       st3(wshift(edt, win * ws), i, e);
       st3(wshift(u1, win * ws), i, o);
+      int j, r;
+      if (po.Uc && packed_mode(G, ix, jy, j, r)) {  // u1 at -k too: the packed input of RHS 2
+        const int mx = mirror_ix(G, ix), my = mirror_jy(G, jy);
+        const size_t im = (size_t)mx * G.ny + my;
+        const double kxm = G.kxf[mx], kym = G.kyf[my];
+        const C3 om = c3add(expL(dt, ld3(Uw, im), G.ph, kxm, kym, pr),
+                            c3scale(dt, expL(dt, compact_at(G, Ac + win * cs, mx, my), G.ph, kxm, kym, pr)));
+        pack_store(G, po, win * cs, j, r, o, om, dmax);
+      }
     }
     flag_nonfinite(o, 1, flags);
   }
+  if (po.Uc) pack_stats_flush(po, dmax);
 }
 
 // stage 2 (integrator.py:99-100): u2 = 3/4 E(dt/2) U + 1/4 E(-dt/2) (u1 + dt A(u1))
 __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, const double2* __restrict__ Ac,
                               Full3w u2, int* flags, int W, size_t ws,
-                              HermGate hg) {
+                              HermGate hg, PackOut po) {
   griddep_wait();
   griddep_launch();
   if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
   const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   const double h = 0.5 * dt;
+  double dmax[3] = {0.0, 0.0, 0.0};
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
     const size_t t = i0 + threadIdx.x;
     C3 o = c3zero();
@@ -1308,14 +1366,26 @@ __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, 
       const size_t win = t / n, i = t - win * n;
       const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
       const double kx = G.kxf[ix], ky = G.kyf[jy];
-      const C3 a = expL(h, ld3(wshift(U, win * ws), i), G.ph, kx, ky, pr);
-      const C3 y = c3add(ld3(wshift(u1, win * ws), i), c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
+      const Full3 Uw = wshift(U, win * ws), u1w = wshift(u1, win * ws);
+      const C3 a = expL(h, ld3(Uw, i), G.ph, kx, ky, pr);
+      const C3 y = c3add(ld3(u1w, i), c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
       const C3 b = expL(-h, y, G.ph, kx, ky, pr);
       o = c3add(c3scale(0.75, a), c3scale(0.25, b));
       st3(wshift(u2, win * ws), i, o);
+      int j, r;
+      if (po.Uc && packed_mode(G, ix, jy, j, r)) {  // u2 at -k too: the packed input of RHS 3
+        const int mx = mirror_ix(G, ix), my = mirror_jy(G, jy);
+        const size_t im = (size_t)mx * G.ny + my;
+        const double kxm = G.kxf[mx], kym = G.kyf[my];
+        const C3 am = expL(h, ld3(Uw, im), G.ph, kxm, kym, pr);
+        const C3 ym = c3add(ld3(u1w, im), c3scale(dt, compact_at(G, Ac + win * cs, mx, my)));
+        const C3 om = c3add(c3scale(0.75, am), c3scale(0.25, expL(-h, ym, G.ph, kxm, kym, pr)));
+        pack_store(G, po, win * cs, j, r, o, om, dmax);
+      }
     }
     flag_nonfinite(o, 2, flags);
   }
+  if (po.Uc) pack_stats_flush(po, dmax);
 }
 
 // stage 3 (integrator.py:101-102): out = 1/3 e_dt + 2/3 E(dt/2) (u2 + dt A(u2))
