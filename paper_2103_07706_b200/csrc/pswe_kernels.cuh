@@ -1028,8 +1028,21 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
   const size_t own = ((size_t)f * GPW + tl) * NX;  // this transform's column in a buffer
   const WLane wl = wlane<NX>(G.twx, t);
   C3 acc[CPT];
+  // the combine's wavenumbers are fixed per thread: loaded once, not per
+  // phase (their L1 latency had been exposed in the combine)
+  // (one ky per CTA when it owns a single column; not at 256, where the
+  // registers would spill)
+  constexpr bool HOIST = NX != 256;
+  constexpr int NKY = GPW == 1 ? 1 : CPT;
+  double kxv[CPT], kyv[NKY];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) acc[c] = c3zero();
+  for (int c = 0; c < CPT; ++c) {
+    acc[c] = c3zero();
+    const int idx = threadIdx.x + c * W::WARPS * 32;
+    const int tt = idx / Kx, r = idx % Kx;
+    if (HOIST) kxv[c] = __ldg(G.kxc + r);
+    if (HOIST && c < NKY) kyv[c] = G.kyc[min(j0 + (NKY == 1 ? 0 : tt), Ky - 1)];
+  }
   // slot (+)= acc: this group's phases (of one window), in chunk order.  A
   // window batch (MW) zero-fills the slots first and flushes at every window
   // boundary into slot [g][window].
@@ -1087,7 +1100,8 @@ __global__ void __launch_bounds__(PassCW<NX>::WARPS * 32, 3)
       const int tt = idx / Kx, r = idx % Kx;
       if (tt < ncol) {
         const double2* Ft = pre + (size_t)tt * NX;  // field f at + f GPW NX
-        const double kx = __ldg(G.kxc + r), ky = G.kyc[j0 + tt];
+        const double kx = HOIST ? kxv[c] : __ldg(G.kxc + r);
+        const double ky = HOIST ? kyv[NKY == 1 ? 0 : c] : G.kyc[j0 + tt];
         const double2 gx = cik(kx, Ft[2 * GPW * NX + r]), gy = cik(ky, Ft[3 * GPW * NX + r]);
         C3 q = {Ft[r], Ft[GPW * NX + r], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
         if (tab) {

@@ -292,7 +292,7 @@ __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WLa
           // twiddle is the lane-uniform constant W_32^c
           const double2 o = v[c];
           const double2 e1 = h ? (INV ? cmk(-o.y, o.x) : cmk(o.y, -o.x)) : recv;
-          const double2 we1 = cmul(w32(c, INV), e1);
+          const double2 we1 = c == 0 ? e1 : cmul(w32(c, INV), e1);  // W_32^0 = 1: exact either way
           v[c] = cadd(e0, we1);
           v[8 + c] = csub(e0, we1);
         }
@@ -337,7 +337,8 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
           // odd lane's DFT16 (sent by the even lane, kept by the odd one), so
           // the odd lane's output factor W_N^{n1} is applied here, to both
           // lanes alike, instead of as a lane-divergent multiply afterwards.
-          const double2 dv = cmul(cmul(csub(a, b), w32(cc, INV)), wn1);
+          const double2 dab = csub(a, b);
+          const double2 dv = cmul(cc == 0 ? dab : cmul(dab, w32(cc, INV)), wn1);
           const double2 send = h ? sv : dv;
           double2 recv;
           recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
