@@ -99,5 +99,21 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// True (warp-uniform) in the last of the CTA's `n` warps to arrive at this
+// point of a round; the counter lives in shared memory and is never reset
+// (callers guarantee that every warp arrives once per round and that no
+// round starts before the previous one completed).  Lets the last consumer
+// of a buffer refill it without a CTA barrier.
+__device__ __forceinline__ bool last_warp_arrival(unsigned* cnt, unsigned n, int lane) {
+  __syncwarp();
+  unsigned last = 0;
+  if (lane == 0) {
+    __threadfence_block();
+    last = atomicAdd(cnt, 1u) % n == n - 1;
+    __threadfence_block();
+  }
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
 
 }  // namespace pswe

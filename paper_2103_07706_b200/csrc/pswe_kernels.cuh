@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
   constexpr int Kx = 2 * (NX / 3) + 1;  // == G.Kx
   const int Ky = G.Ky;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbytes);
+  unsigned* rcnt = reinterpret_cast<unsigned*>(sbytes + 8);  // warps done with the block's buffer
   double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [SLOTS][GPW][Kx]
   double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * W::SLOTS * Kx);
   double* gred = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;  // [WARPS][2]
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
   };
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    *rcnt = 0u;
     fence_mbar_init();
   }
   __syncthreads();
@@ -348,8 +350,12 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
       double2 v[P];
       PSWE_A_GATHER(v, sub)
       if (sub == nsub - 1) {
-        __syncthreads();  // buffer consumed: refill it for the next block while the FFT runs
-        if (f == 0 && blk + (int)gridDim.x < nblk) prefetch(blk + gridDim.x);
+        // buffer consumed: the last warp done with it refills it for the
+        // next block while the FFTs run (no CTA barrier)
+        if (last_warp_arrival(rcnt, W::WARPS, lane) && blk + (int)gridDim.x < nblk) {
+          fence_proxy_async();
+          prefetch(blk + gridDim.x);
+        }
       }
       wfft_t1<NX, true, true>(v, t, xb, wl);
       if (active) store_t1_strided<NX>(v, t, sub ? out1 : out0, 1);
