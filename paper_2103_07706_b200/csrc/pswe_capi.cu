@@ -352,15 +352,22 @@ int launchB_split(pswe_ctx* c, int np, const CUtensorMap& mI1, double2* I2, cuda
 }
 
 template <int NY>
-int launchB_pair(pswe_ctx* c, int np, const CUtensorMap& mI1, const CUtensorMap& mO, cudaStream_t st) {
+int launchB_pair(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUtensorMap& mO, cudaStream_t st) {
   using W = PassBW<NY>;
   const size_t smem = W::template bytes<true>();
   auto kern = passB_pair_kernel<NY>;
   CU(smem_attr(kern, smem, c->device));
-  const int ntp = ((np + 1) / 2) * c->nx;
-  const int blocks = (ntp + W::GPC - 1) / W::GPC;
+  // two phase pairs per CTA when the lanes' pass-B grids hold >= 16 waves of
+  // resident CTAs (512^2 M = 256: 3.811 -> 3.797 ms per RHS, 256^2 M = 256
+  // 870 -> 860 us; with fewer waves the coarser grid's tail costs more, e.g.
+  // 256^2 M = 32 139 -> 148 us)
+  static const int qpc_env = getenv("PSWE_QPC") ? atoi(getenv("PSWE_QPC")) : 0;  // experiments
+  const int npair = (np + 1) / 2;
+  const long long ctas1 = (long long)lanes * npair * (c->nx / W::GPC);
+  const int qpc = std::max(1, qpc_env ? qpc_env : (ctas1 >= 16LL * 3 * c->sms ? 2 : 1));
+  const int blocks = (npair + qpc - 1) / qpc * (c->nx / W::GPC);
   ProfScope ps(c, 1, st);
-  CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), np, mI1, mO));
+  CU(launch_k(c->pdl, kern, blocks, W::WARPS * 32, smem, st, c->grid(), np, mI1, mO, qpc));
   c->launches++;
   c->variant[PSWE_V_PASSB_PAIR]++;
   CU(cudaGetLastError());
@@ -379,7 +386,7 @@ int launchB(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUtens
   if constexpr (NY >= 64) {
     const int sms = c->sms;
     const long long pair_ctas = (long long)lanes * ((np + 1) / 2) * c->nx / PassBW<NY>::GPC;
-    if (passB_fast(c) && pair_ctas >= sms + sms / 3) return launchB_pair<NY>(c, np, mI1, mO, st);
+    if (passB_fast(c) && pair_ctas >= sms + sms / 3) return launchB_pair<NY>(c, np, lanes, mI1, mO, st);
   }
   // fewer single-phase CTAs than SMs: split each row group's transforms over
   // four warps (passB_split_kernel, two transform latencies instead of six)

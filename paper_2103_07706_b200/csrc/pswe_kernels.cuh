@@ -775,7 +775,8 @@ __device__ __forceinline__ void passB_pair_prefetch(int lane, double2* pre, doub
 
 template <int NY>
 __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
-    passB_pair_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mO) {
+    passB_pair_kernel(GridDev Gd, int np, const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mO,
+                      int qpc) {
   griddep_wait();
   griddep_launch();
   using W = PassBW<NY>;
@@ -802,10 +803,12 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(kys + Ky);
   const int nx = Gd.nx;
   const int ntp = ((np + 1) / 2) * nx;  // (phase pair, row) tasks
-  const int first_task = (blockIdx.x * W::WARPS + warp) * GPW;
-  const int t0 = blockIdx.x * R;         // first task of the CTA's tile (one phase pair)
-  const int p0 = 2 * (t0 / nx), x0 = t0 % nx;
-  const int nsub = (p0 + 1 < np) ? 2 : 1;  // CTA-uniform
+  // the CTA's tile: rows x0 .. x0 + R - 1 of the phase pairs pq0 .. pq1 - 1
+  // (qpc pairs per CTA: the prologue, the first gather's latency and the
+  // last store's completion are paid once per qpc pairs)
+  const int rowgroups = nx / R;
+  const int pq0 = (blockIdx.x / rowgroups) * qpc, x0 = (blockIdx.x % rowgroups) * R;
+  const int pq1 = min((np + 1) / 2, pq0 + qpc);
   const int rc = warp * GPW + g;
   const double2* mypre = pre + (size_t)g * 2 * KYA;
   for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
@@ -819,22 +822,27 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   tmem_fence_after_sync();
   const uint32_t taddr = *tslot + ((uint32_t)(32 * warp) << 16);
 
-  // inputs of transform (sub, it): fields (fa, fb) of phases (pa, pb)
-  auto issue = [&](int sub, int it) {
-    const int ph = p0 + sub;
+  // inputs of transform (sub, it) of phase pair pp: fields (fa, fb) of phases (pa, pb)
+  auto issue = [&](int pp, int sub, int it) {
+    const int p0 = 2 * pp, ph = p0 + sub;
+    const bool two = p0 + 1 < np;
     int fa, pa = ph, fb, pb = ph;
     if (it == 0) { fa = 0; fb = 1; }
     else if (it == 1) { fa = 3; fb = 0; }
     else if (it == 2) { fa = 4; fb = 1; }
-    else { fa = 2; fb = nsub == 2 ? 2 : -1; pb = p0 + 1; }
-    passB_pair_prefetch<NY>(lane, pre, preb, bar, &mI, first_task, ntp, nx, fa, pa, fb, pb);
+    else { fa = 2; fb = two ? 2 : -1; pb = p0 + 1; }
+    passB_pair_prefetch<NY>(lane, pre, preb, bar, &mI, pp * nx + x0 + warp * GPW, ntp, nx, fa, pa, fb, pb);
   };
-  issue(0, 0);
+  issue(pq0, 0, 0);
 
   double2 v[P];
   double pa_[P];
   const WLane wl = wlane<NY>(Gd.twy, t);
   uint32_t par = 0;
+#pragma unroll 1
+  for (int pp = pq0; pp < pq1; ++pp) {
+  const int p0 = 2 * pp;
+  const int nsub = (p0 + 1 < np) ? 2 : 1;  // CTA-uniform
 #pragma unroll 1
   for (int sub = 0; sub < nsub; ++sub) {
 #pragma unroll 1
@@ -856,8 +864,10 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
         // nothing after the last ((1,3) reuses the shared depth transform of (0,3))
         const bool last = nsub == 2 ? (sub == 1 && it == 2) : it == 3;
         if (!last) {
-          if (it < 3) issue(sub, it + 1);
-          else issue(sub + 1, 0);
+          if (it < 3) issue(pp, sub, it + 1);
+          else issue(pp, sub + 1, 0);
+        } else if (pp + 1 < pq1) {
+          issue(pp + 1, 0, 0);  // the next pair's first input
         }
         wfft_t1<NY, true, true>(v, t, xb, wl);
       }
@@ -933,6 +943,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
         bulk_commit();
       }
     }
+  }
   }
   if (issuer) bulk_wait0();
   tmem_fence_before_sync();

@@ -516,6 +516,34 @@ def test_latency_paths_are_bitwise_identical(tmp_path):
     assert np.array_equal(outs[0][1], outs[1][1])
 
 
+def test_pairs_per_cta_give_the_same_bits(tmp_path):
+    """Pass B's CTAs may take two phase pairs each (chosen for grids of many
+    waves); scheduling only: one and two pairs per CTA give the same bits at
+    256^2, M = 32 (an odd phase count: the last pair holds one phase)."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2103_07706_b200 as pk\n"
+        "from paper_2103_07706_b200 import cases\n"
+        "c = cases.case_c5(6, 32)\n"
+        "a = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())\n"
+        "np.save(sys.argv[1], np.stack([a.u, a.v, a.eta]))\n" % str(ROOT))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
+    outs = []
+    for q in ("1", "2"):
+        f = tmp_path / f"q{q}.npy"
+        p = subprocess.run([sys.executable, "-c", code, str(f)], env={**base, "PSWE_QPC": q},
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("level", [6, 7])
 def test_single_node_large_grid_matches_oracle(level):
     """One node on 256^2 / 512^2 (apply_nonlinear and the fine-step
