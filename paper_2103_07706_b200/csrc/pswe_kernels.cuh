@@ -184,9 +184,10 @@ struct PassAW {
   // | xbuf per group
   static constexpr int SLOTS = MW ? 9 : 6;
   // ... | the Hermitian gate's per-warp phase maxima [WARPS][2]
+  // ... | kx / 2 [Kx] (the x-derivative fields, see pass A)
   static size_t bytes(int Kx) {
     return 16 + (size_t)GPW * SLOTS * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) +
-           (size_t)WARPS * 2 * sizeof(double);
+           (size_t)WARPS * 2 * sizeof(double) + (size_t)Kx * sizeof(double);
   }
 };
 
@@ -214,6 +215,13 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
   double2* buf = reinterpret_cast<double2*>(sbytes + 16);  // [SLOTS][GPW][Kx]
   double* xbuf = reinterpret_cast<double*>(buf + (size_t)GPW * W::SLOTS * Kx);
   double* gred = xbuf + (size_t)W::WARPS * GPW * WF<NX>::XBUF;  // [WARPS][2]
+  // Half-scaled factors: every quadratic product pass B forms has exactly
+  // one factor among (ux, vx, uy, vy, depth); pass A writes ux, vx and the
+  // depth at half scale (kx / 2, and 1 / (2 nx ny)) and pass B uses ky / 2,
+  // so the products come out halved -- exactly, scaling by 1/2 commutes with
+  // rounding -- and pass B's real-pair unpack needs no multiply by 1/2.
+  double* kxh = gred + 2 * W::WARPS;  // [Kx]
+  for (int r = threadIdx.x; r < Kx; r += blockDim.x) kxh[r] = 0.5 * G.kxc[r];
   const bool tab = ctab != nullptr;
   const int cols = (Ky + GPW - 1) / GPW;
   const int npair = (np + 1) / 2;
@@ -299,7 +307,7 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
         const double2 dep = csub(q.e, bb);
         o[0] = cscale(G.inv_n2, q.u);
         o[fs] = cscale(G.inv_n2, q.v);
-        o[2 * fs] = cscale(G.inv_n2, dep);
+        o[2 * fs] = cscale(0.5 * G.inv_n2, dep);  // half-scaled depth (see kxh)
         if (pscale) {  // (a non-finite input is flagged through pack's statistics: fmax is enough here)
           const double m = fmax(fmax(abs2(q.u), abs2(q.v)), abs2(dep));
           if (sub) gmax1 = fmax(m, gmax1);
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
   if (f >= 3) { /* ikx u', ikx v' */                                                 \
     _Pragma("unroll") for (int n1 = 0; n1 < P; ++n1) {                                 \
       const int r = band_r(t + T * n1, NX, NX / 3, Kx);                                \
-      if (r >= 0) v[n1] = cik(__ldg(G.kxc + r), v[n1]);                                \
+      if (r >= 0) v[n1] = cik(kxh[r], v[n1]);                                          \
     }                                                                                  \
   }
     double2* const out0 = I + ((((size_t)pa) * 5 + f) * Ky + j0 + tl) * NX;
@@ -465,7 +473,9 @@ __device__ __forceinline__ void build_pair(double2* v, int t, const double2* pre
 // after a type-2 forward transform (v[k2] = Z[t + T k2]): split the packed pair
 // into the two real spectra X = (Z + conj Z(-j))/2, Y = (Z - conj Z(-j))/(2i)
 // for j = 0..Ky-1 and store them.
-template <int NY>
+// HALF: the pair's members are at full scale (multiply by 1/2); false: the
+// inputs were formed at half scale (pass A/B's half-scaled factors)
+template <int NY, bool HALF = true>
 __device__ __forceinline__ void unpack_store(const double2* v, int t, double2* outX, double2* outY, int Ky,
                                              int stride, bool active) {
   constexpr int T = WF<NY>::T, P = WF<NY>::P;
@@ -485,8 +495,9 @@ __device__ __forceinline__ void unpack_store(const double2* v, int t, double2* o
     }
     if (active && j < Ky) {
       const double2 a = v[m];
-      outX[(size_t)j * stride] = cmk(0.5 * (a.x + zm.x), 0.5 * (a.y - zm.y));
-      outY[(size_t)j * stride] = cmk(0.5 * (a.y + zm.y), -0.5 * (a.x - zm.x));
+      constexpr double h = HALF ? 0.5 : 1.0;
+      outX[(size_t)j * stride] = cmk(h * (a.x + zm.x), h * (a.y - zm.y));
+      outY[(size_t)j * stride] = cmk(h * (a.y + zm.y), -h * (a.x - zm.x));
     }
   }
 }
@@ -569,7 +580,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   const size_t KyNX = (size_t)Ky * Gd.nx;
   double2* out = I2 + (size_t)pl * 4 * KyNX + x;  // I2[pl][f][j][x]
   const double2* mypre = pre + (size_t)g * 2 * KYA;
-  for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
+  for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = 0.5 * Gd.kyc[i];  // half-scaled uy, vy
 
   if (lane == 0) {
     mbar_init(bar, 1);
@@ -614,7 +625,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
     if (it < 2) continue;
     wfft_t2<NY, false>(v, t, xb, wl);
     const int fo = it == 2 ? 0 : 2;
-    unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
+    unpack_store<NY, false>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
   }
 }
 
@@ -664,7 +675,7 @@ __global__ void __launch_bounds__(128)
   const int pl = active ? task / Gd.nx : 0, x = active ? task % Gd.nx : 0;
   const size_t KyNX = (size_t)Ky * Gd.nx;
   double2* out = I2 + (size_t)pl * 4 * KyNX + x;
-  for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
+  for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = 0.5 * Gd.kyc[i];  // half-scaled uy, vy
   if (lane == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -698,7 +709,7 @@ __global__ void __launch_bounds__(128)
   }
   wfft_t2<NY, false>(v, t, xb, wl);
   const int fo = warp == 0 ? 0 : 2;
-  unpack_store<NY>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
+  unpack_store<NY, false>(v, t, out + (size_t)fo * KyNX, out + (size_t)(fo + 1) * KyNX, Ky, Gd.nx, active);
 }
 
 // Unpack a forward pair transform (as unpack_store) into the warp pair's staging
@@ -737,10 +748,10 @@ __device__ __forceinline__ void unpack_stage(const double2* v, int t, double2* s
       r.y = __shfl_sync(0xffffffffu, src.y, (T - t) & (T - 1), T);
       zm = t == 0 ? v[(P - m) & (P - 1)] : r;
     }
-    if (j < Ky) {
+    if (j < Ky) {  // inputs at half scale (pass A/B's half-scaled factors): no 1/2 here
       const double2 a = v[m];
-      stage[stage_slot<NY, R>(j, rc)] = cmk(0.5 * (a.x + zm.x), 0.5 * (a.y - zm.y));
-      stage[stage_slot<NY, R>(Ky + j, rc)] = cmk(0.5 * (a.y + zm.y), -0.5 * (a.x - zm.x));
+      stage[stage_slot<NY, R>(j, rc)] = cmk(a.x + zm.x, a.y - zm.y);
+      stage[stage_slot<NY, R>(Ky + j, rc)] = cmk(a.y + zm.y, zm.x - a.x);
     }
   }
 }
@@ -811,7 +822,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
   const int pq1 = min((np + 1) / 2, pq0 + qpc);
   const int rc = warp * GPW + g;
   const double2* mypre = pre + (size_t)g * 2 * KYA;
-  for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = Gd.kyc[i];
+  for (int i = threadIdx.x; i < Ky; i += blockDim.x) kys[i] = 0.5 * Gd.kyc[i];  // half-scaled uy, vy
   if (lane == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
