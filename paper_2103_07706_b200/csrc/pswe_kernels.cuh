@@ -184,10 +184,10 @@ struct PassAW {
   // | xbuf per group
   static constexpr int SLOTS = MW ? 9 : 6;
   // ... | the Hermitian gate's per-warp phase maxima [WARPS][2]
-  // ... | kx / 2 [Kx] (the x-derivative fields, see pass A)
+  // ... | kx / 2 [Kx] (the x-derivative fields, see pass A) | kx [Kx]
   static size_t bytes(int Kx) {
     return 16 + (size_t)GPW * SLOTS * Kx * sizeof(double2) + (size_t)WARPS * GPW * WF<NX>::XBUF * sizeof(double) +
-           (size_t)WARPS * 2 * sizeof(double) + (size_t)Kx * sizeof(double);
+           (size_t)WARPS * 2 * sizeof(double) + (size_t)2 * Kx * sizeof(double);
   }
 };
 
@@ -221,7 +221,11 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
   // so the products come out halved -- exactly, scaling by 1/2 commutes with
   // rounding -- and pass B's real-pair unpack needs no multiply by 1/2.
   double* kxh = gred + 2 * W::WARPS;  // [Kx]
-  for (int r = threadIdx.x; r < Kx; r += blockDim.x) kxh[r] = 0.5 * G.kxc[r];
+  double* kxs = kxh + Kx;              // [Kx] kx for the exponentials (shared, not L1 loads)
+  for (int r = threadIdx.x; r < Kx; r += blockDim.x) {
+    kxs[r] = G.kxc[r];
+    kxh[r] = 0.5 * kxs[r];
+  }
   const bool tab = ctab != nullptr;
   const int cols = (Ky + GPW - 1) / GPW;
   const int npair = (np + 1) / 2;
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(PassAW<NX, MW>::WARPS * 32, PassAW<NX, MW>::CT
       double2* e = buf + idx;
       const C3 q0 = {e[0], e[fs], e[2 * fs]};
       const double2 bb = e[3 * fs];
-      const double kx = __ldg(G.kxc + r);
+      const double kx = kxs[r];
       double ky = kyb[0];
 #pragma unroll
       for (int c = 1; c < GPW; ++c)

@@ -326,7 +326,11 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
       } else {
         const int h = t & 1, n1 = t >> 1;
         const double2 wn1 = wsel(wl.wn1(), INV);  // W_N^{n1}
-        // s_c = a + b, d_c = (a - b) W_32^c for this lane's c = 8h + cc
+        // s_c = a + b, d_c = (a - b) W_32^c for this lane's c = 8h + cc.  The
+        // combined twiddles W_32^cc W_N^{n1} by the three-term recurrence
+        // z_{cc+1} = 2 cos(2 pi / 32) z_cc - z_{cc-1} (two FMAs each)
+        constexpr double C32 = 1.96157056080646086074;  // 2 cos(2 pi / 32)
+        double2 zp = wn1, zc = cmul(w32(1, INV), wn1);
         double2 q[16];
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
@@ -338,7 +342,15 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
           // the odd lane's output factor W_N^{n1} is applied here, to both
           // lanes alike, instead of as a lane-divergent multiply afterwards.
           const double2 dab = csub(a, b);
-          const double2 dv = cmul(cc == 0 ? dab : cmul(dab, w32(cc, INV)), wn1);
+          double2 tw = wn1;
+          if (cc == 1) tw = zc;
+          if (cc >= 2) {
+            const double2 zn = cmk(fma(C32, zc.x, -zp.x), fma(C32, zc.y, -zp.y));
+            zp = zc;
+            zc = zn;
+            tw = zn;
+          }
+          const double2 dv = cmul(dab, tw);
           const double2 send = h ? sv : dv;
           double2 recv;
           recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
