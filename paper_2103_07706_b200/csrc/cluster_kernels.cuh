@@ -51,8 +51,14 @@ struct CFusedW {
   static constexpr size_t ACC_BYTES = (size_t)3 * JL * Kx * sizeof(double2);
   static constexpr size_t KY_BYTES = ((size_t)Ky * sizeof(double) + 15) / 16 * 16;
   static constexpr size_t SCR_BYTES = (size_t)GPW * WF<N>::XBUF * sizeof(double);
-  // I | R (stage A: e^{sL} U; stage B: physical stash) | exchange buffers | ACC | ky | idle scratch
-  static constexpr size_t bytes() { return I_BYTES + R_BYTES + XB_BYTES + ACC_BYTES + KY_BYTES + SCR_BYTES; }
+  // my modes' U (u, v, eta) and b, cached once per kernel (one window), and kx
+  static constexpr size_t UC_BYTES = (size_t)4 * JL * Kx * sizeof(double2);
+  static constexpr size_t KX_BYTES = ((size_t)Kx * sizeof(double) + 15) / 16 * 16;
+  static constexpr int MI = (JL * Kx + NT - 1) / NT;  // modes per thread (at most)
+  // I | R (stage A: e^{sL} U; stage B: physical stash) | exchange buffers | ACC | ky | idle scratch | U, b | kx
+  static constexpr size_t bytes() {
+    return I_BYTES + R_BYTES + XB_BYTES + ACC_BYTES + KY_BYTES + SCR_BYTES + UC_BYTES + KX_BYTES;
+  }
   static_assert(WF<N>::XBUF <= 2 * LD, "exchange buffer must fit in a column");
 };
 
@@ -80,6 +86,10 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
   double* kys = reinterpret_cast<double*>(q);
   q += W::KY_BYTES;
   double* idle = reinterpret_cast<double*>(q);
+  q += W::SCR_BYTES;
+  double2* UCc = reinterpret_cast<double2*>(q);  // [4][JL][Kx]: u, v, eta, b of my modes
+  q += W::UC_BYTES;
+  double* kxs = reinterpret_cast<double*>(q);
   // every CTA's columns, by rank (distributed shared memory)
   // column (f, j) of its owner CTA (mapa per access: no per-rank pointer table in local memory)
   auto colp = [&](int f, int j) -> double2* {
@@ -95,7 +105,36 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
   const bool tab = ctab != nullptr;
   const WLane wlx = wlane<N>(G.twx, t), wly = wlane<N>(G.twy, t);
   for (int i = threadIdx.x; i < Ky; i += NT) kys[i] = G.kyc[i];
+  for (int i = threadIdx.x; i < Kx; i += NT) kxs[i] = G.kxc[i];
   const int nmode = jl_n * Kx;  // my compact modes
+  constexpr int MI = W::MI;
+  // one window: my modes' U and b stay in shared memory for all phases
+  // (window batches read each phase's window state from global memory)
+  if constexpr (!MW) {
+    for (int m = threadIdx.x; m < nmode; m += NT) {
+      const int jl = m / Kx, r = m % Kx, idx = (rank + C * jl) * Kx + r;
+      const size_t e = (size_t)jl * Kx + r;
+      UCc[e] = Uc[idx];
+      UCc[JL * Kx + e] = Uc[KyKx + idx];
+      UCc[2 * JL * Kx + e] = Uc[2 * KyKx + idx];
+      UCc[3 * JL * Kx + e] = G.bc[idx];
+    }
+  }
+  // each thread's modes m = tid + k NT: their (c1, c2) phase-table entries
+  // for the next phase are loaded a whole phase ahead (and reused by the
+  // combine), so no table load sits on a phase's critical path
+  double2 c12n[MI];
+  auto load_c12 = [&](int p) {
+#pragma unroll
+    for (int k = 0; k < MI; ++k) {
+      const int m = threadIdx.x + k * NT;
+      c12n[k] = czero();
+      if (ctab && p < hi && m < nmode) {
+        const int jl = m / Kx, r = m % Kx;
+        c12n[k] = __ldg(ctab + (size_t)p * KyKx + (size_t)(rank + C * jl) * Kx + r);
+      }
+    }
+  };
 
   auto zero_acc = [&]() {
     for (int idx = threadIdx.x; idx < 3 * JL * Kx; idx += NT) ACC[idx] = czero();
@@ -111,6 +150,7 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
   };
   zero_acc();
   int wcur = MW && lo < hi ? ph.win[lo] : 0;
+  load_c12(lo);
   __syncthreads();
 
 #pragma unroll 1
@@ -125,17 +165,24 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
     }
     const double s = ph.s[p], w = ph.w[p];
     const double2* U = Uc + (MW ? (size_t)ph.win[p] * ph.ustride : 0);
-    const double2* ct = tab ? ctab + (size_t)p * KyKx : nullptr;
+    double2 c12c[MI];
+#pragma unroll
+    for (int k = 0; k < MI; ++k) c12c[k] = c12n[k];
+    load_c12(p + 1);
     // ---- A: e^{sL} U of my columns' modes, scaled by 1/(nx ny)
     double gmax = 0.0;
-    for (int m = threadIdx.x; m < nmode; m += NT) {
+#pragma unroll
+    for (int k = 0; k < MI; ++k) {
+      const int m = threadIdx.x + k * NT;
+      if (m >= nmode) break;
       const int jl = m / Kx, r = m % Kx, j = rank + C * jl;
       const int idx = j * Kx + r;
-      const C3 q0 = {U[idx], U[KyKx + idx], U[2 * KyKx + idx]};
-      const double kx = __ldg(G.kxc + r), ky = kys[j];
-      const C3 qe = tab ? exp_c12(ct[idx], q0, G.ph, kx, ky) : expL(s, q0, G.ph, kx, ky, pr);
-      const double2 dep = csub(qe.e, G.bc[idx]);
       const size_t e = (size_t)jl * Kx + r;
+      const C3 q0 = MW ? C3{U[idx], U[KyKx + idx], U[2 * KyKx + idx]}
+                       : C3{UCc[e], UCc[JL * Kx + e], UCc[2 * JL * Kx + e]};
+      const double kx = kxs[r], ky = kys[j];
+      const C3 qe = tab ? exp_c12(c12c[k], q0, G.ph, kx, ky) : expL(s, q0, G.ph, kx, ky, pr);
+      const double2 dep = csub(qe.e, MW ? G.bc[idx] : UCc[3 * JL * Kx + e]);
       EU[e] = cscale(G.inv_n2, qe.u);
       EU[JL * Kx + e] = cscale(G.inv_n2, qe.v);
       EU[2 * JL * Kx + e] = cscale(G.inv_n2, dep);
@@ -160,7 +207,7 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
 #pragma unroll
         for (int n1 = 0; n1 < P; ++n1) {
           const int r = band_r(t + T * n1, N, N / 3, Kx);
-          if (r >= 0) v[n1] = cik(__ldg(G.kxc + r), v[n1]);
+          if (r >= 0) v[n1] = cik(kxs[r], v[n1]);
         }
       }
       double2* col = I + ((size_t)f * JL + jl) * LD;
@@ -257,14 +304,17 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
     }
     __syncthreads();
     // combine my modes: flux divergence, e^{-sL}, weight; ascending phase order
-    for (int m = threadIdx.x; m < nmode; m += NT) {
+#pragma unroll
+    for (int k = 0; k < MI; ++k) {
+      const int m = threadIdx.x + k * NT;
+      if (m >= nmode) break;
       const int jl = m / Kx, r = m % Kx, j = rank + C * jl;
       const double2* F = I + (size_t)jl * LD + r;  // field f at + f JL LD
-      const double kx = __ldg(G.kxc + r), ky = kys[j];
+      const double kx = kxs[r], ky = kys[j];
       const double2 gx = cik(kx, F[2 * JL * LD]), gy = cik(ky, F[3 * JL * LD]);
       C3 qq = {F[0], F[JL * LD], cmk(-(gx.x + gy.x), -(gx.y + gy.y))};
       if (tab) {
-        double2 c12 = ct[j * Kx + r];
+        double2 c12 = c12c[k];
         c12.x = -c12.x;  // e^{-sL}: c1(-s) = -c1(s), c2(-s) = c2(s)
         qq = exp_c12(c12, qq, G.ph, kx, ky);
       } else {
