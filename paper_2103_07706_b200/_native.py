@@ -277,34 +277,30 @@ def upload_fields(arrays, device: int, band_ctx=None):
     ent = cache.get(key)
     if ent is None:
         pin = torch.empty((len(arrays),) + shape, dtype=torch.complex128, pin_memory=True)
-        ent = [pin, pin.numpy(), [None] * len(arrays)]
+        # per slot: its last DMA's event (created once, re-recorded per call)
+        ent = [pin, pin.numpy(), [torch.cuda.Event() for _ in arrays], [False] * len(arrays)]
         cache[key] = ent
-    pin, pn, evs = ent
+    pin, pn, evs, used = ent
     dev = torch.device("cuda", device)
     out = torch.empty((len(arrays),) + shape, dtype=torch.complex128, device=dev)
     cur = torch.cuda.current_stream(dev)
     # staged on the host: whole fields (one threaded copy per field costs
     # less than several copies of the band's blocks -- the copies are
     # dispatch-bound); on the bus: the band only
-    blocks = [(slice(None), slice(None))]
     for i, a in enumerate(arrays):
-        if evs[i] is not None:
+        if used[i]:
             evs[i].synchronize()
-        fast = a.dtype == np.complex128 and a.flags.writeable and all(st >= 0 for st in a.strides)
-        src = torch.from_numpy(a) if fast else None
-        for r, c in blocks:
-            if fast:
-                pin[i, r, c].copy_(src[r, c])
-            else:  # read-only / negative strides / other dtypes: numpy's copy
-                np.copyto(pn[i, r, c], a[r, c], casting="same_kind")
+        if a.dtype == np.complex128 and a.flags.writeable and all(st >= 0 for st in a.strides):
+            pin[i].copy_(torch.from_numpy(a))
+        else:  # read-only / negative strides / other dtypes: numpy's copy
+            np.copyto(pn[i], a, casting="same_kind")
         if band_ctx is not None:
             _check(_lib.pswe_copy_band(band_ctx.h, 0, _ptrs([out[i].data_ptr()]), _ptrs([pin[i].data_ptr()]), 1,
                                        ctypes.c_void_p(cur.cuda_stream)))
         else:
             out[i].copy_(pin[i], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(cur)
-        evs[i] = ev
+        evs[i].record(cur)
+        used[i] = True
     return [out[i] for i in range(len(arrays))]
 
 

@@ -80,15 +80,14 @@ torch.cuda.synchronize()
 arrays = [c.state.u, c.state.v, c.state.eta]
 key = ((n, n), 3, ctx.device)
 ent = _native._PIN.__dict__["in"][key]
-pinb, pn, evs = ent
+pinb, pn, evs, _used = ent
 T = {}
 for _ in range(20):
     t = [time.perf_counter()]
     out = torch.empty((3, n, n), dtype=torch.complex128, device="cuda")
     t.append(time.perf_counter())
     for i, a in enumerate(arrays):
-        if evs[i] is not None:
-            evs[i].synchronize()
+        evs[i].synchronize()
         t.append(time.perf_counter())
         src = torch.from_numpy(a)
         pinb[i].copy_(src)
@@ -97,9 +96,7 @@ for _ in range(20):
                                                    _native._ptrs([pinb[i].data_ptr()]), 1,
                                                    ctypes.c_void_p(st.cuda_stream)))
         t.append(time.perf_counter())
-        ev = torch.cuda.Event()
-        ev.record(st)
-        evs[i] = ev
+        evs[i].record(st)
         t.append(time.perf_counter())
     d = np.diff(t) * 1e3
     for k, v in enumerate(d):
