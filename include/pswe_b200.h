@@ -93,6 +93,15 @@ int pswe_averaged_tendency(pswe_ctx* ctx, const double* u_dev, const double* v_d
                            const double* eta_dev, double* du_dev, double* dv_dev, double* deta_dev,
                            void* stream);
 
+/* Same, and the result's 2/3 band (everything that can be nonzero: the
+ * tendency is dealiased) copied into three pinned host buffers of the full
+ * (nx, ny) layout before the call's single synchronisation -- the drop-in
+ * call's device-to-host leg (averaging.py:116-156 returns host arrays).
+ * Host entries outside the band are not touched. */
+int pswe_averaged_tendency_band_d2h(pswe_ctx* ctx, const double* u_dev, const double* v_dev,
+                                    const double* eta_dev, double* du_dev, double* dv_dev, double* deta_dev,
+                                    double* const* host3, void* stream);
+
 /* N(U) alone (apply_nonlinear, dynamics.py:139-176), full layout. */
 int pswe_apply_nonlinear(pswe_ctx* ctx, const double* u_dev, const double* v_dev,
                          const double* eta_dev, double* du_dev, double* dv_dev, double* deta_dev,

@@ -49,6 +49,7 @@ SIGNATURES = {
     "pswe_unpack": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_averaged_tendency_compact": (_i, [_vp, _vp, _vp, _vp]),
     "pswe_averaged_tendency": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pswe_averaged_tendency_band_d2h": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_apply_nonlinear": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_apply_linear": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_propagate": (_i, [_vp, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -232,6 +233,19 @@ def band_hosts_async(shape, count: int):
             _zero_out_of_band(h, shape[0], shape[1])
         return hs
     return _filler().submit(make)
+
+
+def band_hosts_split(shape, count: int):
+    """Pinned host buffers for a band download, taken now, and a future
+    that zero-fills their out-of-band part on a helper thread -- disjoint
+    from the band the device copies into them, so both may run at once."""
+    hs = [_POOL_OUT.take(shape, _torch().complex128) for _ in range(count)]
+
+    def fill():
+        for h in hs:
+            _zero_out_of_band(h, shape[0], shape[1])
+
+    return hs, _filler().submit(fill)
 
 
 def download_fields(tensors, band_ctx=None, hosts=None):
@@ -448,6 +462,15 @@ class Context:
 
     def averaged_tendency(self, U):
         return self._call3(_lib.pswe_averaged_tendency, U)
+
+    def averaged_tendency_to_host(self, U, hosts):
+        """The averaged tendency of device fields U, its 2/3 band copied
+        into the pinned host tensors `hosts` within the call's single
+        synchronisation; returns numpy views of `hosts`."""
+        out = [self.empty_full() for _ in range(3)]
+        _check(_lib.pswe_averaged_tendency_band_d2h(self.h, *(_dptr(x) for x in U), *(_dptr(x) for x in out),
+                                                    _ptrs([h.data_ptr() for h in hosts]), _stream(self.torch)))
+        return [_POOL_OUT.array(h) for h in hosts]
 
     def averaged_tendency_compact(self, Uc, out=None):
         out = self.empty_compact() if out is None else out

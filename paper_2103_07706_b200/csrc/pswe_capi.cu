@@ -1466,9 +1466,17 @@ int pswe_averaged_tendency_compact(pswe_ctx* c, const double* Uc, double* Ac, vo
 // full layout in, with the gate: pack (+ statistics), evaluation over the
 // nodes (s_dev, P) with the gate's verdict, unpack, synchronise, and the
 // exact check when flagged (node-wrapped message when `k` is given)
+static int copy_band(pswe_ctx* c, int dir, double* const* dst, const double* const* src, int nfields,
+                     cudaStream_t st);
+struct ConstPtr3 {
+  const double* p[3];
+  operator const double* const*() const { return p; }
+};
+static ConstPtr3 f3c(const double* a, const double* b, const double* e) { return ConstPtr3{{a, b, e}}; }
+
 static int gated_rhs(pswe_ctx* c, const double* u, const double* v, const double* e, double* du, double* dv,
                      double* de, const PhaseSet& ps, const std::vector<double>& s_host, const std::vector<int>* k,
-                     cudaStream_t st) {
+                     cudaStream_t st, double* const* host3 = nullptr) {
   CU(cudaSetDevice(c->device));
   TRY(ensure_compact(c));
   TRY(ensure_hgate(c, ps.P));
@@ -1485,6 +1493,9 @@ static int gated_rhs(pswe_ctx* c, const double* u, const double* v, const double
   c->launches++;
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(c->flags_host, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  // the drop-in call's band download joins the same synchronisation (the
+  // exact gate, when the bound cannot decide, only validates the result)
+  if (host3) TRY(copy_band(c, 1, host3, f3c(du, dv, de), 3, st));
   CU(cudaStreamSynchronize(st));
   if (*c->flags_host & (1 << HERM_BIT_RHS)) return exact_gate(c, ps.s, s_host, k, f3(u, v, e), st);
   return PSWE_OK;
@@ -1496,6 +1507,16 @@ int pswe_averaged_tendency(pswe_ctx* c, const double* u, const double* v, const 
   if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
   TRY(check_nodes(c));
   return gated_rhs(c, u, v, e, du, dv, de, quad_phases(c), c->s_live, &c->k_live, (cudaStream_t)stream);
+}
+
+int pswe_averaged_tendency_band_d2h(pswe_ctx* c, const double* u, const double* v, const double* e, double* du,
+                                    double* dv, double* de, double* const* host3, void* stream) {
+  if (!c || !u || !v || !e || !du || !dv || !de || !host3) return set_err(PSWE_EINVAL, "null argument");
+  for (int f = 0; f < 3; ++f)
+    if (!host3[f]) return set_err(PSWE_EINVAL, "null host buffer");
+  if (!c->quad_set) return set_err(PSWE_ESTATE, "no quadrature set (pswe_set_quadrature)");
+  TRY(check_nodes(c));
+  return gated_rhs(c, u, v, e, du, dv, de, quad_phases(c), c->s_live, &c->k_live, (cudaStream_t)stream, host3);
 }
 
 int pswe_apply_nonlinear(pswe_ctx* c, const double* u, const double* v, const double* e, double* du, double* dv,
@@ -1900,6 +1921,11 @@ int pswe_copy_band(pswe_ctx* c, int dir, double* const* dst, const double* const
   if (!c || !dst || !src || nfields < 0) return set_err(PSWE_EINVAL, "null argument");
   if (dir != 0 && dir != 1) return set_err(PSWE_EINVAL, "dir must be 0 (host to device) or 1 (device to host)");
   CU(cudaSetDevice(c->device));
+  return copy_band(c, dir, dst, src, nfields, (cudaStream_t)stream);
+}
+
+static int copy_band(pswe_ctx* c, int dir, double* const* dst, const double* const* src, int nfields,
+                     cudaStream_t stream) {
   const cudaMemcpyKind kind = dir == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
   const size_t pitch = (size_t)c->ny * 2 * sizeof(double);
   // rows |wx| <= kxm and columns |wy| <= kym: two row blocks x two column blocks
