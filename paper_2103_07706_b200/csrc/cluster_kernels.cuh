@@ -55,9 +55,12 @@ struct CFusedW {
   static constexpr size_t UC_BYTES = (size_t)4 * JL * Kx * sizeof(double2);
   static constexpr size_t KX_BYTES = ((size_t)Kx * sizeof(double) + 15) / 16 * 16;
   static constexpr int MI = (JL * Kx + NT - 1) / NT;  // modes per thread (at most)
+  // stage A's outputs pushed to the row owners: [5][Ky][RLD], my rows
+  static constexpr int RLD = ROWS + 1;
+  static constexpr size_t IR_BYTES = (size_t)5 * Ky * RLD * sizeof(double2);
   // I | R (stage A: e^{sL} U; stage B: physical stash) | exchange buffers | ACC | ky | idle scratch | U, b | kx
   static constexpr size_t bytes() {
-    return I_BYTES + R_BYTES + XB_BYTES + ACC_BYTES + KY_BYTES + SCR_BYTES + UC_BYTES + KX_BYTES;
+    return I_BYTES + R_BYTES + XB_BYTES + ACC_BYTES + KY_BYTES + SCR_BYTES + UC_BYTES + KX_BYTES + IR_BYTES;
   }
   static_assert(WF<N>::XBUF <= 2 * LD, "exchange buffer must fit in a column");
 };
@@ -90,6 +93,12 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
   double2* UCc = reinterpret_cast<double2*>(q);  // [4][JL][Kx]: u, v, eta, b of my modes
   q += W::UC_BYTES;
   double* kxs = reinterpret_cast<double*>(q);
+  q += W::KX_BYTES;
+  // stage B's inputs, my rows of every column: stage A's CTAs store them
+  // here remotely (distributed shared memory stores do not stall the
+  // writer), so stage B reads locally instead of issuing remote loads
+  double2* IR = reinterpret_cast<double2*>(q);  // [5][Ky][RLD]
+  constexpr int RLD = W::RLD, ROWS = W::ROWS;
   // every CTA's columns, by rank (distributed shared memory)
   // column (f, j) of its owner CTA (mapa per access: no per-rank pointer table in local memory)
   auto colp = [&](int f, int j) -> double2* {
@@ -212,8 +221,14 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
       }
       double2* col = I + ((size_t)f * JL + jl) * LD;
       wfft_t1<N, true, true>(v, t, active ? reinterpret_cast<double*>(col) : idle + (size_t)gi * WF<N>::XBUF, wlx);
-      __syncwarp();
-      if (active) store_t1_strided<N>(v, t, col, 1);
+      if (active) {  // row x of column j -> its owner (x / ROWS), local row x % ROWS
+        const int j = rank + C * jl;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const int x = t1_pos<N>(t, i);
+          *cluster.map_shared_rank(IR + ((size_t)f * Ky + j) * RLD + x % ROWS, (unsigned)(x / ROWS)) = v[i];
+        }
+      }
     }
     cluster.sync();  // every CTA's columns complete
     // ---- B: my rows; warp role `it` of its row group
@@ -234,10 +249,11 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
           continue;
         }
         const int jj = lo_ ? k : N - k;
-        const double2 A = colp(fa, jj)[x];
+        const int xl = x - rank * ROWS;
+        const double2 A = IR[((size_t)fa * Ky + jj) * RLD + xl];
         double2 B = czero();
         if (fb >= 0) {
-          B = colp(fb, jj)[x];
+          B = IR[((size_t)fb * Ky + jj) * RLD + xl];
           if (it == 1 || it == 2) B = cik(kys[jj], B);
         }
         v[n1] = (k == 0) ? cmk(A.x, B.x) : (lo_ ? cmk(A.x - B.y, A.y + B.x) : cmk(A.x + B.y, B.x - A.y));
