@@ -519,7 +519,8 @@ def test_latency_paths_are_bitwise_identical(tmp_path):
 def test_pairs_per_cta_give_the_same_bits(tmp_path):
     """Pass B's CTAs may take two phase pairs each (chosen for grids of many
     waves); scheduling only: one and two pairs per CTA give the same bits at
-    256^2, M = 32 (an odd phase count: the last pair holds one phase)."""
+    256^2 for M = 32 (an odd phase count: the last pair holds one phase) and
+    M = 5 (an odd pair count: the last CTA row holds one pair)."""
     import os
     import subprocess
     import sys
@@ -530,9 +531,13 @@ def test_pairs_per_cta_give_the_same_bits(tmp_path):
         "import sys, numpy as np; sys.path.insert(0, %r)\n"
         "import paper_2103_07706_b200 as pk\n"
         "from paper_2103_07706_b200 import cases\n"
-        "c = cases.case_c5(6, 32)\n"
-        "a = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())\n"
-        "np.save(sys.argv[1], np.stack([a.u, a.v, a.eta]))\n" % str(ROOT))
+        "outs = []\n"
+        "for M in (32, 5):\n"
+        "    c = cases.case_c5(6, 32)\n"
+        "    q = pk.kernel_weights(c.quadrature.T, M)\n"
+        "    a = pk.averaged_tendency(c.state, q, c.params, pk.PropagatorSpec.exact())\n"
+        "    outs.append(np.stack([a.u, a.v, a.eta]))\n"
+        "np.save(sys.argv[1], np.stack(outs))\n" % str(ROOT))
     base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
     outs = []
     for q in ("1", "2"):
