@@ -399,7 +399,7 @@ int launchB(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUtens
 }
 
 template <int NX>
-int pass_c_groups(const pswe_ctx* c, int CP) {
+int pass_c_groups(const pswe_ctx* c, int CP, int lanes) {
   // phase groups per chunk: the grid (cols x Gc CTAs) should fill whole waves
   // of the resident CTAs (occupancy query), each CTA keeping >= 4 phases to amortise its
   // prologue and slot update.  Pick the Gc with the best wave efficiency.
@@ -414,7 +414,14 @@ int pass_c_groups(const pswe_ctx* c, int CP) {
   // a grid that cannot fill the SMs even at 4 phases per CTA is latency-
   // bound: then down to one phase per CTA (64^2, M = 8: pass C 16 -> 9 us)
   const int gmax = (long long)cols * std::max(1, CP / 4) < sms ? CP : std::max(1, CP / 4);
-  for (int g = 1; g <= gmax && g <= 16; ++g) {
+  // all lanes' slots within 64 MiB (512^2, four lanes: at most 5 groups of
+  // 2.8 MB slots, the choice there is unchanged); small grids, whose few
+  // column blocks would otherwise leave most SMs idle (64^2: 3 column blocks
+  // x 16 groups = 48 CTAs for 511 phases), may use up to 256 groups (64^2
+  // M = 128 76 -> 66 us, 128^2 M = 256 255 -> 245 us, C3 step 188 -> 178 us)
+  const size_t slot_bytes = c->compact_elems() * sizeof(double2) * (size_t)std::max(1, lanes);
+  const int gcap = (int)std::max<size_t>(1, std::min<size_t>(256, ((size_t)64 << 20) / slot_bytes));
+  for (int g = 1; g <= gmax && g <= gcap; ++g) {
     const int ctas = cols * g;
     const int waves = (ctas + slots - 1) / slots;
     const double eff = (double)ctas / ((double)waves * slots);
@@ -477,15 +484,15 @@ int dispatchB(pswe_ctx* c, int np, int lanes, const CUtensorMap& mI1, const CUte
   }
   return set_err(PSWE_EUNSUPPORTED, "unsupported ny = %d", c->ny);
 }
-int groupsC(const pswe_ctx* c, int CP) {
+int groupsC(const pswe_ctx* c, int CP, int lanes) {
   switch (c->nx) {
-    case 8: return pass_c_groups<8>(c, CP);
-    case 16: return pass_c_groups<16>(c, CP);
-    case 32: return pass_c_groups<32>(c, CP);
-    case 64: return pass_c_groups<64>(c, CP);
-    case 128: return pass_c_groups<128>(c, CP);
-    case 256: return pass_c_groups<256>(c, CP);
-    default: return pass_c_groups<512>(c, CP);
+    case 8: return pass_c_groups<8>(c, CP, lanes);
+    case 16: return pass_c_groups<16>(c, CP, lanes);
+    case 32: return pass_c_groups<32>(c, CP, lanes);
+    case 64: return pass_c_groups<64>(c, CP, lanes);
+    case 128: return pass_c_groups<128>(c, CP, lanes);
+    case 256: return pass_c_groups<256>(c, CP, lanes);
+    default: return pass_c_groups<512>(c, CP, lanes);
   }
 }
 
@@ -876,7 +883,8 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
   nchunks = (nchunks + lanes - 1) / lanes * lanes;
   const int CP = std::max(1, std::min(P, (P + nchunks - 1) / nchunks));
   nchunks = (P + CP - 1) / CP;
-  const int Gc = c->gen ? gen_groups(c, CP) : groupsC(c, CP);  // accumulation slots = phase groups per chunk
+  const int Gc = c->gen ? gen_groups(c, CP) : groupsC(c, CP, lanes);  // accumulation slots = phase groups per chunk
+  const int SGN = Gc;
   c->pdl = pdl_enabled() && nchunks == 1;
   const size_t cw = (size_t)ps.W * c->compact_elems();  // one slot set: W compact states
   TRY(c->inter.alloc(per_phase * CP * lanes));
@@ -938,8 +946,16 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
   if (!direct) {
     const size_t n = cw;
     ProfScope ps(c, 3, st);
-    CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, n), 256, 0, st, (const double2*)c->slots.p, lanes * Gc, n,
-                Ac));
+    // many slots (small grids): the split reduction (64^2 M = 256: 113 -> 104 us
+    // with the raised group cap; up to 32 slots the one-pass kernel is faster)
+    if (lanes * SGN > 32) {
+      const int blocks = (int)std::min<size_t>((n + 31) / 32, (size_t)c->sms * 8);
+      CU(launch_k(c->pdl, reduce_slots_split_kernel, blocks, 32 * RED_PARTS, 0, st, (const double2*)c->slots.p,
+                  lanes * SGN, n, Ac));
+    } else {
+      CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, n), 256, 0, st, (const double2*)c->slots.p, lanes * SGN,
+                  n, Ac));
+    }
     c->launches++;
     c->variant[PSWE_V_REDUCE]++;
     CU(cudaGetLastError());

@@ -1179,6 +1179,47 @@ __global__ void reduce_slots_kernel(const double2* __restrict__ slots, int Gc, s
   }
 }
 
+// The same sum for many slots (small grids, whose pass C runs many phase
+// groups): the Gc slots are split into RP contiguous ranges, warp r of a
+// block sums range r for 32 consecutive entries (coalesced), and warp 0 adds
+// the RP range sums in order -- a fixed summation tree, so still bitwise
+// deterministic, and RP times fewer dependent load batches per thread.
+constexpr int RED_PARTS = 8;
+__global__ void __launch_bounds__(32 * RED_PARTS) reduce_slots_split_kernel(const double2* __restrict__ slots,
+                                                                          int Gc, size_t n,
+                                                                          double2* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ double2 part[RED_PARTS][32];
+  const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;
+  const int per = (Gc + RED_PARTS - 1) / RED_PARTS;
+  const int g0 = r * per, g1 = min(Gc, g0 + per);
+  for (size_t base = (size_t)blockIdx.x * 32; base < n; base += (size_t)gridDim.x * 32) {
+    const size_t i = base + lane;
+    double2 a = czero();
+    if (i < n) {
+      constexpr int B = 8;
+      for (int g = g0; g < g1; g += B) {
+        double2 v[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) v[k] = g + k < g1 ? slots[(size_t)(g + k) * n + i] : czero();
+#pragma unroll
+        for (int k = 0; k < B; ++k)
+          if (g + k < g1) a = (g + k == g0) ? v[k] : cadd(a, v[k]);
+      }
+    }
+    part[r][lane] = a;
+    __syncthreads();
+    if (r == 0 && i < n) {
+      double2 t = part[0][lane];
+      for (int q = 1; q < RED_PARTS; ++q)
+        if (q * per < Gc) t = cadd(t, part[q][lane]);
+      out[i] = t;
+    }
+    __syncthreads();
+  }
+}
+
 // ============================================================================
 // layout conversion full <-> compact
 // ============================================================================
