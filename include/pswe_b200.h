@@ -161,6 +161,14 @@ double pswe_max_frequency(const pswe_ctx* ctx);
 /* Number of kernels this context has launched (instrumentation). */
 int64_t pswe_launch_count(const pswe_ctx* ctx);
 
+/* Debug (environment PSWE_DEBUG_GUARD set before the first allocation):
+ * every context buffer carries 64 KiB NaN-filled guard bands on both sides.
+ * Synchronises the device and returns the number of live guarded buffers and
+ * of guard bands found changed (including those of buffers freed since).
+ * Without PSWE_DEBUG_GUARD both are 0.  A memcheck stand-in; no reference
+ * counterpart. */
+int pswe_debug_check_guards(int64_t* guarded, int64_t* damaged);
+
 /* Launches per kernel variant (instrumentation: which code path ran), graph
  * replays included.  Variants: */
 #define PSWE_V_PASSA 0        /* pass A (e^{sL} + inverse x-FFTs) */

@@ -60,6 +60,7 @@ SIGNATURES = {
     "pswe_window_batch_run": (_i, [_vp, _d, _i, _vp, _c_int_p, _vp]),
     "pswe_max_frequency": (_d, [_vp]),
     "pswe_launch_count": (ctypes.c_int64, [_vp]),
+    "pswe_debug_check_guards": (_i, [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "pswe_variant_launches": (_i, [_vp, ctypes.POINTER(ctypes.c_int64), _i]),
     "pswe_diagnostics": (_i, [_vp, _vp, _vp, _vp, ctypes.POINTER(_d), _vp]),
     "pswe_to_physical": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
@@ -567,6 +568,14 @@ class Context:
 
 _ctx_cache: dict = {}
 _ctx_lock = threading.Lock()
+
+
+def debug_check_guards() -> tuple[int, int]:
+    """(guarded buffers, damaged guard bands) under PSWE_DEBUG_GUARD
+    (pswe_debug_check_guards; synchronises the device); (0, 0) otherwise."""
+    g, d = ctypes.c_int64(), ctypes.c_int64()
+    _check(load_library().pswe_debug_check_guards(ctypes.byref(g), ctypes.byref(d)))
+    return int(g.value), int(d.value)
 
 
 def release_thread_contexts() -> None:

@@ -65,6 +65,41 @@ std::recursive_mutex g_capture_mutex;
 // have moved is re-captured
 std::atomic<int64_t> g_alloc_gen{0};
 
+// Debug guard bands (PSWE_DEBUG_GUARD, read once): every context buffer is
+// allocated with GUARD_BYTES of 0xFF bytes (fp64 NaN) on both sides and
+// registered here.  A kernel writing past a buffer's ends changes a guard
+// (pswe_debug_check_guards counts them); one reading past them picks up
+// NaNs that reach its output.  The memcheck stand-in where compute-sanitizer
+// is unavailable.
+constexpr size_t GUARD_BYTES = 64 << 10;
+bool guard_enabled() {
+  static const bool on = getenv("PSWE_DEBUG_GUARD") != nullptr;
+  return on;
+}
+struct GuardedBlock {
+  unsigned char* base;
+  size_t bytes;  // payload between the guards
+};
+std::mutex g_guard_mutex;
+std::vector<GuardedBlock> g_guarded;
+int64_t g_guard_hits = 0;  // corrupted guard bands found at free time
+
+// number of corrupted guard bands of one block (synchronises the device)
+int guard_damage(const GuardedBlock& b) {
+  std::vector<unsigned char> h(GUARD_BYTES);
+  int bad = 0;
+  for (int side = 0; side < 2; ++side) {
+    const unsigned char* src = side == 0 ? b.base : b.base + GUARD_BYTES + b.bytes;
+    if (cudaMemcpy(h.data(), src, GUARD_BYTES, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+    for (size_t i = 0; i < GUARD_BYTES; ++i)
+      if (h[i] != 0xFF) {
+        ++bad;
+        break;
+      }
+  }
+  return bad;
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -73,18 +108,46 @@ struct DevBuf {
     if (count <= n) return PSWE_OK;
     std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
     ++g_alloc_gen;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    CU(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    free_();
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (guard_enabled()) {
+      unsigned char* base = nullptr;
+      CU(cudaMalloc(&base, bytes + 2 * GUARD_BYTES));
+      CU(cudaMemset(base, 0xFF, GUARD_BYTES));
+      CU(cudaMemset(base + GUARD_BYTES + bytes, 0xFF, GUARD_BYTES));
+      CU(cudaDeviceSynchronize());
+      p = reinterpret_cast<T*>(base + GUARD_BYTES);
+      std::lock_guard<std::mutex> gl(g_guard_mutex);
+      g_guarded.push_back({base, bytes});
+    } else {
+      CU(cudaMalloc(&p, bytes));
+    }
     n = count;
     return PSWE_OK;
   }
-  void release() {
-    std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
-    if (p) cudaFree(p);
+  void free_() {
+    if (p && guard_enabled()) {
+      unsigned char* base = reinterpret_cast<unsigned char*>(p) - GUARD_BYTES;
+      {
+        std::lock_guard<std::mutex> gl(g_guard_mutex);
+        for (size_t i = 0; i < g_guarded.size(); ++i)
+          if (g_guarded[i].base == base) {
+            cudaDeviceSynchronize();
+            g_guard_hits += guard_damage(g_guarded[i]);
+            g_guarded.erase(g_guarded.begin() + i);
+            break;
+          }
+      }
+      cudaFree(base);
+    } else if (p) {
+      cudaFree(p);
+    }
     p = nullptr;
     n = 0;
+  }
+  void release() {
+    std::lock_guard<std::recursive_mutex> lock(g_capture_mutex);
+    free_();
   }
 };
 
@@ -1868,6 +1931,20 @@ done:
 double pswe_max_frequency(const pswe_ctx* c) { return c ? c->lam_max : 0.0; }
 
 int64_t pswe_launch_count(const pswe_ctx* c) { return c ? c->launches : 0; }
+
+int pswe_debug_check_guards(int64_t* guarded, int64_t* damaged) {
+  if (!guarded || !damaged) return set_err(PSWE_EINVAL, "null argument");
+  *guarded = 0;
+  *damaged = 0;
+  if (!guard_enabled()) return PSWE_OK;
+  CU(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> gl(g_guard_mutex);
+  int64_t bad = g_guard_hits;
+  for (const GuardedBlock& b : g_guarded) bad += guard_damage(b);
+  *guarded = (int64_t)g_guarded.size();
+  *damaged = bad;
+  return PSWE_OK;
+}
 
 int pswe_variant_launches(const pswe_ctx* c, int64_t* counts, int n) {
   if (!c || !counts) return set_err(PSWE_EINVAL, "null argument");

@@ -568,13 +568,53 @@ def test_single_node_large_grid_matches_oracle(level):
     assert v["passB_split"] > 0
 
 
-def test_poisoned_scratch_gives_the_same_bits(tmp_path):
-    """Stand-in for compute-sanitizer's initcheck/racecheck (closed on the
-    GPU pool): with every intermediate, slot and the output NaN-filled before
-    each evaluation (PSWE_DEBUG_POISON), every kernel variant -- split,
-    row and paired pass B, one and four lanes, one and many chunks and pass-C
-    groups -- must produce the same bits as without, so no entry is read
-    before it is written and no read races its producer."""
+_VARIANT_WORKLOAD = (
+    "import sys, json, numpy as np; sys.path.insert(0, %r)\n"
+    "import paper_2103_07706_b200 as pk\n"
+    "from paper_2103_07706_b200 import cases, _native\n"
+    "outs, var = [], {}\n"
+    "for r, M in ((3, 256), (4, 8), (5, 4), (5, 32), (6, 128), (7, 8), (7, 64)):\n"
+    "    c = cases.case_c5(r, M)\n"
+    "    ctx = pk.dynamics.context(c.state, c.params)\n"
+    "    ctx.set_propagator('exact')\n"
+    "    ctx.set_quadrature(c.quadrature.s, c.quadrature.w)\n"
+    "    Uc = ctx.pack(pk.dynamics.upload(ctx, c.state))\n"
+    "    for _ in range(3):\n"
+    "        outs.append(ctx.averaged_tendency_compact(Uc).cpu().numpy())\n"
+    "    for k, v in ctx.variant_launches.items(): var[k] = var.get(k, 0) + v\n"
+    "c = cases.case_c2()\n"
+    "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
+    "tr = pk.run(c.state, cfg, c.params, t_end=4 * c.dt)\n"
+    "s = tr.states[-1]\n"
+    "outs.append(np.stack([s.u, s.v, s.eta]))\n"
+    "outs.append(np.array(pk.device_diagnostics(s, c.params)))\n"
+    "g = pk.make_grid(64, 32, 4.0e7, 2.0e7)\n"
+    "rng = np.random.default_rng(9)\n"
+    "f = lambda sc: pk.dealias(g, pk.to_spectral(g, sc * rng.standard_normal((64, 32))))\n"
+    "st = pk.State(grid=g, u=f(1.0), v=f(1.0), eta=f(50.0))\n"
+    "p = pk.PhysicsParams(f=1e-4, g=9.8, H=5960.0, b=np.zeros((64, 32), complex))\n"
+    "ctx = pk.dynamics.context(st, p)\n"
+    "for _ in range(2):\n"
+    "    a = pk.averaged_tendency(st, pk.kernel_weights(3600.0, 256), p, pk.PropagatorSpec.exact())\n"
+    "    outs.append(np.stack([a.u, a.v, a.eta]))\n"
+    "for k, v in ctx.variant_launches.items(): var[k] = var.get(k, 0) + v\n"
+    "g = pk.make_grid(48, 48, 4.0e7, 4.0e7)\n"
+    "f = lambda sc: pk.dealias(g, pk.to_spectral(g, sc * rng.standard_normal((48, 48))))\n"
+    "st = pk.State(grid=g, u=f(1.0), v=f(1.0), eta=f(50.0))\n"
+    "p = pk.PhysicsParams(f=1e-4, g=9.8, H=5960.0, b=np.zeros((48, 48), complex))\n"
+    "a = pk.averaged_tendency(st, pk.kernel_weights(3600.0, 16), p, pk.PropagatorSpec.exact())\n"
+    "outs.append(np.stack([a.u, a.v, a.eta]))\n"
+    "c = cases.case_c3()\n"
+    "ws = pk.window_sweep(c.state, c.params, c.dt, 2 * c.dt, [0.0, 1800.0, 3600.0], M=4)\n"
+    "for w in ws: outs.append(np.stack([w.final.u, w.final.v, w.final.eta]))\n"
+    "np.savez(sys.argv[1], *outs)\n"
+    "gd, dm = _native.debug_check_guards()\n"
+    "print(json.dumps({'var': var, 'guards': [gd, dm]}))\n")
+
+
+def _variant_runs(tmp_path, envs):
+    """Run the variant workload in fresh processes, one per environment;
+    returns [(outputs, launches per variant, (guarded buffers, damaged guards))]."""
     import json
     import os
     import subprocess
@@ -582,49 +622,52 @@ def test_poisoned_scratch_gives_the_same_bits(tmp_path):
 
     from conftest import ROOT
 
-    code = (
-        "import sys, json, numpy as np; sys.path.insert(0, %r)\n"
-        "import paper_2103_07706_b200 as pk\n"
-        "from paper_2103_07706_b200 import cases\n"
-        "outs, var = [], {}\n"
-        "for r, M in ((3, 256), (4, 8), (5, 4), (5, 32), (6, 128), (7, 8), (7, 64)):\n"
-        "    c = cases.case_c5(r, M)\n"
-        "    ctx = pk.dynamics.context(c.state, c.params)\n"
-        "    ctx.set_propagator('exact')\n"
-        "    ctx.set_quadrature(c.quadrature.s, c.quadrature.w)\n"
-        "    Uc = ctx.pack(pk.dynamics.upload(ctx, c.state))\n"
-        "    for _ in range(3):\n"
-        "        outs.append(ctx.averaged_tendency_compact(Uc).cpu().numpy())\n"
-        "    for k, v in ctx.variant_launches.items(): var[k] = var.get(k, 0) + v\n"
-        "c = cases.case_c2()\n"
-        "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
-        "s = pk.run(c.state, cfg, c.params, t_end=4 * c.dt).states[-1]\n"
-        "outs.append(np.stack([s.u, s.v, s.eta]))\n"
-        "g = pk.make_grid(64, 32, 4.0e7, 2.0e7)\n"
-        "rng = np.random.default_rng(9)\n"
-        "f = lambda sc: pk.dealias(g, pk.to_spectral(g, sc * rng.standard_normal((64, 32))))\n"
-        "st = pk.State(grid=g, u=f(1.0), v=f(1.0), eta=f(50.0))\n"
-        "p = pk.PhysicsParams(f=1e-4, g=9.8, H=5960.0, b=np.zeros((64, 32), complex))\n"
-        "ctx = pk.dynamics.context(st, p)\n"
-        "for _ in range(2):\n"
-        "    a = pk.averaged_tendency(st, pk.kernel_weights(3600.0, 256), p, pk.PropagatorSpec.exact())\n"
-        "    outs.append(np.stack([a.u, a.v, a.eta]))\n"
-        "for k, v in ctx.variant_launches.items(): var[k] = var.get(k, 0) + v\n"
-        "np.savez(sys.argv[1], *outs)\n"
-        "print(json.dumps(var))\n" % str(ROOT))
+    code = _VARIANT_WORKLOAD % str(ROOT)
     base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
     res = []
-    for i, env in enumerate(({}, {"PSWE_DEBUG_POISON": "1"})):
+    for i, env in enumerate(envs):
         f = tmp_path / f"p{i}.npz"
         p = subprocess.run([sys.executable, "-c", code, str(f)], env={**base, **env},
                            capture_output=True, text=True, timeout=600)
         assert p.returncode == 0, p.stderr
-        var = json.loads(p.stdout.strip().splitlines()[-1])
+        info = json.loads(p.stdout.strip().splitlines()[-1])
         with np.load(f) as z:
-            res.append([z[k] for k in z.files])
+            res.append(([z[k] for k in z.files], info["var"], tuple(info["guards"])))
+    return res
+
+
+def test_poisoned_scratch_gives_the_same_bits(tmp_path):
+    """Stand-in for compute-sanitizer's initcheck/racecheck (closed on the
+    GPU pool): with every intermediate, slot and the output NaN-filled before
+    each evaluation (PSWE_DEBUG_POISON), every kernel variant -- split,
+    row and paired pass B, one and four lanes, one and many chunks and pass-C
+    groups -- must produce the same bits as without, so no entry is read
+    before it is written and no read races its producer."""
+    res = _variant_runs(tmp_path, ({}, {"PSWE_DEBUG_POISON": "1"}))
+    var = res[1][1]
     for name in ("passB_split", "passB_row", "passB_pair", "reduce", "fused"):
         assert var[name] > 0, (name, var)
-    for a, b in zip(res[0], res[1]):
+    for a, b in zip(res[0][0], res[1][0]):
+        assert np.all(np.isfinite(b))
+        assert np.array_equal(a, b)
+
+
+def test_guard_bands_stay_intact(tmp_path):
+    """Stand-in for compute-sanitizer's memcheck (closed on the GPU pool,
+    profiles/sanitizer_closed_r02.log): with PSWE_DEBUG_GUARD every context
+    buffer (tables, intermediates, slots, stepper and diagnostics scratch)
+    sits between 64 KiB NaN guard bands.  Over every kernel family -- the
+    three passes in all their variants, fused and cluster small-grid kernels,
+    generic mixed-radix sizes, the stepper and graph replay, diagnostics, the
+    window batch -- no guard may change (no write past a buffer's ends) and
+    the results must keep their bits (no read past them: it would bring in
+    NaNs)."""
+    res = _variant_runs(tmp_path, ({}, {"PSWE_DEBUG_GUARD": "1"}))
+    assert res[0][2] == (0, 0)
+    guarded, damaged = res[1][2]
+    assert guarded >= 20, guarded
+    assert damaged == 0
+    for a, b in zip(res[0][0], res[1][0]):
         assert np.all(np.isfinite(b))
         assert np.array_equal(a, b)
 
