@@ -128,4 +128,24 @@ __device__ __forceinline__ C3 exp_c12(double2 c12, const C3& q, const Phys& p, d
   return c3add(c3add(q, c3scale(c12.x, l1)), c3scale(c12.y, l2));
 }
 
+// (c1, c2) of the exact exponential at time t for a mode (as exp_exact forms
+// them).  A mode and its mirror -k share omega (|k|^2 is sign-blind, bit for
+// bit), and c1(-t) = -c1(t), c2(-t) = c2(t): one sincos serves all the
+// exponentials a stage kernel's thread applies.
+__device__ __forceinline__ double2 c12_of(const Phys& p, double kx, double ky, double t) {
+  const double om = omega_of(p, kx, ky);
+  if (om > 0.0) {
+    double sn, cs;
+    sincos(om * t, &sn, &cs);
+    return cmk(sn / om, (1.0 - cs) / (om * om));
+  }
+  return cmk(t, 0.5 * t * t);
+}
+
+// e^{tL} q by the context's route, with (c1, c2) precomputed for the exact route
+__device__ __forceinline__ C3 expLc(double2 c12, double t, const C3& q, const Phys& p, double kx, double ky,
+                                    const Prop& pr) {
+  return pr.kind == 0 ? exp_c12(c12, q, p, kx, ky) : exp_cheb(t, q, p, kx, ky, pr);
+}
+
 }  // namespace pswe

@@ -1416,8 +1416,9 @@ __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const doub
       const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
       const double kx = G.kxf[ix], ky = G.kyf[jy];
       const Full3 Uw = wshift(U, win * ws);
-      const C3 e = expL(dt, ld3(Uw, i), G.ph, kx, ky, pr);
-      const C3 ea = expL(dt, compact_at(G, Ac + win * cs, ix, jy), G.ph, kx, ky, pr);
+      const double2 cd = pr.kind == 0 ? c12_of(G.ph, kx, ky, dt) : czero();  // this mode and its mirror
+      const C3 e = expLc(cd, dt, ld3(Uw, i), G.ph, kx, ky, pr);
+      const C3 ea = expLc(cd, dt, compact_at(G, Ac + win * cs, ix, jy), G.ph, kx, ky, pr);
       o = c3add(e, c3scale(dt, ea));
       st3(wshift(edt, win * ws), i, e);
       st3(wshift(u1, win * ws), i, o);
@@ -1426,8 +1427,8 @@ __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const doub
         const int mx = mirror_ix(G, ix), my = mirror_jy(G, jy);
         const size_t im = (size_t)mx * G.ny + my;
         const double kxm = G.kxf[mx], kym = G.kyf[my];
-        const C3 om = c3add(expL(dt, ld3(Uw, im), G.ph, kxm, kym, pr),
-                            c3scale(dt, expL(dt, compact_at(G, Ac + win * cs, mx, my), G.ph, kxm, kym, pr)));
+        const C3 om = c3add(expLc(cd, dt, ld3(Uw, im), G.ph, kxm, kym, pr),
+                            c3scale(dt, expLc(cd, dt, compact_at(G, Ac + win * cs, mx, my), G.ph, kxm, kym, pr)));
         pack_store(G, po, win * cs, j, r, o, om, dmax);
       }
     }
@@ -1454,9 +1455,10 @@ __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, 
       const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
       const double kx = G.kxf[ix], ky = G.kyf[jy];
       const Full3 Uw = wshift(U, win * ws), u1w = wshift(u1, win * ws);
-      const C3 a = expL(h, ld3(Uw, i), G.ph, kx, ky, pr);
+      const double2 ch = pr.kind == 0 ? c12_of(G.ph, kx, ky, h) : czero(), cm = cmk(-ch.x, ch.y);  // +-dt/2
+      const C3 a = expLc(ch, h, ld3(Uw, i), G.ph, kx, ky, pr);
       const C3 y = c3add(ld3(u1w, i), c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
-      const C3 b = expL(-h, y, G.ph, kx, ky, pr);
+      const C3 b = expLc(cm, -h, y, G.ph, kx, ky, pr);
       o = c3add(c3scale(0.75, a), c3scale(0.25, b));
       st3(wshift(u2, win * ws), i, o);
       int j, r;
@@ -1464,9 +1466,9 @@ __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, 
         const int mx = mirror_ix(G, ix), my = mirror_jy(G, jy);
         const size_t im = (size_t)mx * G.ny + my;
         const double kxm = G.kxf[mx], kym = G.kyf[my];
-        const C3 am = expL(h, ld3(Uw, im), G.ph, kxm, kym, pr);
+        const C3 am = expLc(ch, h, ld3(Uw, im), G.ph, kxm, kym, pr);
         const C3 ym = c3add(ld3(u1w, im), c3scale(dt, compact_at(G, Ac + win * cs, mx, my)));
-        const C3 om = c3add(c3scale(0.75, am), c3scale(0.25, expL(-h, ym, G.ph, kxm, kym, pr)));
+        const C3 om = c3add(c3scale(0.75, am), c3scale(0.25, expLc(cm, -h, ym, G.ph, kxm, kym, pr)));
         pack_store(G, po, win * cs, j, r, o, om, dmax);
       }
     }

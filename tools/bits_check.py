@@ -19,6 +19,13 @@ c = cases.case_c3()
 cfg = pk.StepConfig(dt=1800.0, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())
 s = pk.step_averaged_ssprk3(c.state, cfg, c.params)
 res["C3step"] = np.stack([s.u, s.v, s.eta])
+c = cases.case_c2()
+cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())
+s = pk.run(c.state, cfg, c.params, t_end=4 * c.dt).states[-1]
+res["C2run"] = np.stack([s.u, s.v, s.eta])
+c = cases.case_c3()
+for w in pk.window_sweep(c.state, c.params, c.dt, 2 * c.dt, [0.0, 1800.0, 3600.0], M=4):
+    res[f"win{w.T:g}"] = np.stack([w.final.u, w.final.v, w.final.eta])
 np.savez(sys.argv[1], **res)
 if len(sys.argv) > 2:
     ref = np.load(sys.argv[2])
