@@ -575,7 +575,9 @@ def run_ours(args, ws, rank, local):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded planar C5 stand-in, SURVEY.md 8d)",
-            "config": workload_config(case) | {"parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+            # config: the workload only, identical to the reference arm's line
+            "config": workload_config(case),
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
             "roofline": roofline, "rhs_roofline": rhs_roofline, "fp64": fp64, "kernels": kern,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "gpu": torch.cuda.get_device_name(local), "sweep": sweep, "step_configs": steps_info,
