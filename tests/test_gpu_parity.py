@@ -158,16 +158,20 @@ def test_c5_benchmarked_rhs_matches_oracle(level, M):
     assert err <= RHS_TOL
 
 
+@pytest.mark.parametrize("M", [8, 32, 128, 256])
 @pytest.mark.parametrize("level", [4, 5, 6, 7])
-def test_c5_m128_unbalanced_matches_oracle(level):
-    """C5 states are balanced (e^{sL} U = U), which would hide a wrong phase
-    shift in pass A; here an unbalanced, band-limited perturbation of O(1)
-    relative size is added, so every phase's forward and backward
-    exponential matters.  M = 128 (255 phases): several chunks per lane,
-    every lane, phase pairs, several pass-C slots."""
-    c = cases.case_c5(level, 128)
+def test_c5_sweep_point_unbalanced_matches_oracle(level, M):
+    """Every point of the C5 throughput sweep (refinements 4-7 x M in {8, 32,
+    128, 256}: all 16 entries of bench.py's `sweep`), all 2M - 1 live phases
+    against the oracle's node sum.  C5 states are balanced (e^{sL} U = U),
+    which would hide a wrong phase shift in pass A; here an unbalanced,
+    band-limited perturbation of O(1) relative size is added, so every
+    phase's forward and backward exponential matters.  The points cover the
+    cluster kernel (64^2, M <= 32), one-chunk chains, and several chunks per
+    lane on every lane with phase pairs and several pass-C slots."""
+    c = cases.case_c5(level, M)
     g = c.grid
-    rng = np.random.default_rng(100 + level)
+    rng = np.random.default_rng(100 + level + 1000 * (M != 128) * M)
     S = O.Setup(g.nx, g.ny, g.Lx, g.Ly, c.params.f, c.params.g, c.params.H)
     U = arr(c.state)
     pert = np.stack([O.truncate(O.spectral(rng.standard_normal((g.nx, g.ny))), S.mask) for _ in range(3)])
@@ -176,7 +180,7 @@ def test_c5_m128_unbalanced_matches_oracle(level):
     U = U + pert
     got = pk.averaged_tendency(state_from(U, g), c.quadrature, c.params, pk.PropagatorSpec.exact())
     err = O.rel_l2(arr(got), _oracle_rhs(c, U))
-    print(f"C5 {g.nx}^2 M=128 unbalanced rel L2 vs oracle {err:.3e}")
+    print(f"C5 {g.nx}^2 M={M} unbalanced rel L2 vs oracle {err:.3e}")
     assert err <= RHS_TOL
 
 
