@@ -201,11 +201,11 @@ __global__ void __launch_bounds__(FusedW<N>::NT)
       fused_pair<N, true, true>(v, t, fld(3), fld(0), kys);  // (ux, i ky u)
       wfft_t1<N, true, true>(v, t, xb, wly);
 #pragma unroll
-      for (int i = 0; i < P; ++i) pa[i] = -(uv[i].x * v[i].x + uv[i].y * v[i].y);  // A = -(u ux + v uy)
+      for (int i = 0; i < P; ++i) pa[i] = ndot(uv[i], v[i]);  // A = -(u ux + v uy)
       fused_pair<N, true, true>(v, t, fld(4), fld(1), kys);  // (vx, i ky v)
       wfft_t1<N, true, true>(v, t, xb, wly);
 #pragma unroll
-      for (int i = 0; i < P; ++i) v[i] = cmk(pa[i], -(uv[i].x * v[i].x + uv[i].y * v[i].y));  // + iB
+      for (int i = 0; i < P; ++i) v[i] = cmk(pa[i], ndot(uv[i], v[i]));  // + iB
       wfft_t2<N, false>(v, t, xb, wly);
       __syncwarp();  // the row's (u, v) inputs were read by every lane of the group
       unpack_store<N>(v, t, const_cast<double2*>(fld(0)), const_cast<double2*>(fld(1)), Ky, LD, active);

@@ -14,6 +14,20 @@ namespace pswe {
 
 // ---------------------------------------------------------------- complex
 __device__ __forceinline__ double2 cmk(double x, double y) { return make_double2(x, y); }
+// -x as a sign-bit flip on the integer pipe.  A negation whose consumer cannot
+// take an operand modifier (a select, shuffle or store) otherwise costs a DADD
+// on the fp64 pipe, the pipe that bounds the FFT passes.  Bitwise equal to it.
+__device__ __forceinline__ double dneg(double x) {
+  return __hiloint2double(__double2hiint(x) ^ (int)0x80000000u, __double2loint(x));
+}
+// x with its sign flipped when flip != 0 (no select, no fp64 instruction)
+__device__ __forceinline__ double dflip(double x, bool flip) {
+  return __hiloint2double(__double2hiint(x) ^ (int)((unsigned)flip << 31), __double2loint(x));
+}
+// -(a.x b.x + a.y b.y) with the negation folded into the operands, so no
+// DADD is spent on it: fma(-a.x, b.x, -(a.y b.y)), bitwise equal to
+// negating fma(a.x, b.x, a.y b.y)
+__device__ __forceinline__ double ndot(double2 a, double2 b) { return __fma_rn(-a.x, b.x, -__dmul_rn(a.y, b.y)); }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return cmk(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return cmk(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cscale(double s, double2 a) { return cmk(s * a.x, s * a.y); }

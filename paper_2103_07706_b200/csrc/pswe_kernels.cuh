@@ -611,13 +611,13 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         const double2 q = uv[i * T + t];
-        pa[i] = -(q.x * v[i].x + q.y * v[i].y);  // A = -(u ux + v uy)
+        pa[i] = ndot(q, v[i]);  // A = -(u ux + v uy)
       }
     } else if (it == 2) {
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         const double2 q = uv[i * T + t];
-        v[i] = cmk(pa[i], -(q.x * v[i].x + q.y * v[i].y));  // A + iB, B = -(u vx + v vy)
+        v[i] = cmk(pa[i], ndot(q, v[i]));  // A + iB, B = -(u vx + v vy)
       }
     } else {
 #pragma unroll
@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(128)
     const double2 q = suv[i * 32 + lane];
     if (warp == 0) {
       const double2 a = sux[i * 32 + lane], b = svx[i * 32 + lane];
-      v[i] = cmk(-(q.x * a.x + q.y * a.y), -(q.x * b.x + q.y * b.y));  // A + iB
+      v[i] = cmk(ndot(q, a), ndot(q, b));  // A + iB
     } else {
       const double d = sd[i * 32 + lane].x;
       v[i] = cmk(q.x * d, q.y * d);  // C + iD = u depth + i v depth
@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
           double2 q[4];
           uv_get4<NY, true>(q, nullptr, taddr, i0, t);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) pa_[i0 + k] = -(q[k].x * v[i0 + k].x + q[k].y * v[i0 + k].y);
+          for (int k = 0; k < 4; ++k) pa_[i0 + k] = ndot(q[k], v[i0 + k]);
         }
         tmem_stash16d(taddr + 64, pa_);
         PSWE_ST_WAIT_EARLY();
@@ -914,7 +914,7 @@ __global__ void __launch_bounds__(PassBW<NY>::WARPS * 32, 3)
 #pragma unroll
           for (int k = 0; k < 4; ++k)  // A + iB, B = -(u vx + v vy)
             v[i0 + k] = cmk(__hiloint2double(r[2 * k + 1], r[2 * k]),
-                            -(q[k].x * v[i0 + k].x + q[k].y * v[i0 + k].y));
+                            ndot(q[k], v[i0 + k]));
         }
       } else {
         if (sub == 0) {

@@ -146,9 +146,10 @@ __device__ __forceinline__ void apply_powers_(double2* v, double2 w, bool neg) {
     const double2 w2 = cmul(w, w);
     const double c2 = 2.0 * w2.x;
     const bool ng = NEG && neg;
-    double2 po = ng ? cmk(-w.x, -w.y) : w, pom = ng ? cmk(-w.x, w.y) : cmk(w.x, -w.y);
-    double2 pe = ng ? cmk(-w2.x, -w2.y) : w2, pem = cmk(ng ? -1.0 : 1.0, 0.0);
-    if constexpr (NEG) v[0] = neg ? cmk(-v[0].x, -v[0].y) : v[0];
+    // sign flips on the integer pipe (dflip / dneg), not DADDs
+    double2 po = cmk(dflip(w.x, ng), dflip(w.y, ng)), pom = cmk(po.x, -po.y);
+    double2 pe = cmk(dflip(w2.x, ng), dflip(w2.y, ng)), pem = cmk(ng ? -1.0 : 1.0, 0.0);
+    if constexpr (NEG) v[0] = cmk(dflip(v[0].x, neg), dflip(v[0].y, neg));
 #pragma unroll
     for (int k = 1; k < L; k += 2) {
       v[k] = cmul(v[k], po);
@@ -291,7 +292,7 @@ __device__ __forceinline__ void wfft_t1(double2* v, int t, double* xb, const WLa
           // E_1[8 + c] = v[c] is rotated (a register swap + sign) and the
           // twiddle is the lane-uniform constant W_32^c
           const double2 o = v[c];
-          const double2 e1 = h ? (INV ? cmk(-o.y, o.x) : cmk(o.y, -o.x)) : recv;
+          const double2 e1 = h ? (INV ? cmk(dneg(o.y), o.x) : cmk(o.y, dneg(o.x))) : recv;
           const double2 we1 = c == 0 ? e1 : cmul(w32(c, INV), e1);  // W_32^0 = 1: exact either way
           v[c] = cadd(e0, we1);
           v[8 + c] = csub(e0, we1);
@@ -359,13 +360,13 @@ __device__ __forceinline__ void wfft_t2(double2* v, int t, double* xb, const WLa
           // (received value in the upper half for both lanes: one select
           // instead of two); the rotation multiplies its output k by (-1)^k,
           // undone by negating the twiddle base below.
-          q[cc] = h ? (INV ? cmk(-dv.y, dv.x) : cmk(dv.y, -dv.x)) : sv;
+          q[cc] = h ? (INV ? cmk(dneg(dv.y), dv.x) : cmk(dv.y, dneg(dv.x))) : sv;
           q[8 + cc] = recv;
         }
         dft16<INV>(q);  // Z[n1][2 q' + h] (the odd lane's times W^{n1} (-1)^q')
         // twiddle W_N^{n1 (2q'+h)} = W^{n1 h} (W^{2 n1})^{q'}
         double2 wb = wsel(wl.w2n1(), INV);
-        if (h) wb = cmk(-wb.x, -wb.y);
+        wb = cmk(dflip(wb.x, h), dflip(wb.y, h));
         apply_powers<16>(q, wb);
         PSWE_XPOSE(
             for (int k = 0; k < 16; ++k) xb[n1 * S + 2 * k + h] = q[k].x,
