@@ -915,8 +915,13 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
     TRY(rc);
     if (!direct) {
       ProfScope pr3(c, 3, st);
-      CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, cw), 256, 0, st, (const double2*)c->slots.p, Gc, cw,
-                  Ac));
+      // 32 slots per load round (staged kernel) instead of the serial batches
+      if (!getenv("PSWE_NO_STAGED"))
+        CU(launch_k(c->pdl, reduce_slots_staged_kernel, (int)std::min<size_t>((cw + 31) / 32, (size_t)c->sms * 8), 256,
+                    0, st, (const double2*)c->slots.p, Gc, cw, Ac));
+      else
+        CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, cw), 256, 0, st, (const double2*)c->slots.p, Gc, cw,
+                    Ac));
       c->launches++;
       c->variant[PSWE_V_REDUCE]++;
       CU(cudaGetLastError());
@@ -1015,6 +1020,10 @@ int rhs_compact(pswe_ctx* c, const PhaseSet& ps, const double2* Uc, double2* Ac,
       const int blocks = (int)std::min<size_t>((n + 31) / 32, (size_t)c->sms * 8);
       CU(launch_k(c->pdl, reduce_slots_split_kernel, blocks, 32 * RED_PARTS, 0, st, (const double2*)c->slots.p,
                   lanes * SGN, n, Ac));
+    } else if (n <= (size_t(1) << 16) && !getenv("PSWE_NO_STAGED")) {
+      // small states: every slot loaded in one round, same summation order
+      CU(launch_k(c->pdl, reduce_slots_staged_kernel, (int)std::min<size_t>((n + 31) / 32, (size_t)c->sms * 8), 256, 0,
+                  st, (const double2*)c->slots.p, lanes * SGN, n, Ac));
     } else {
       CU(launch_k(c->pdl, reduce_slots_kernel, elem_grid(c, n), 256, 0, st, (const double2*)c->slots.p, lanes * SGN,
                   n, Ac));

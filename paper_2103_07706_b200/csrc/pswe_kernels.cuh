@@ -1179,6 +1179,41 @@ __global__ void reduce_slots_kernel(const double2* __restrict__ slots, int Gc, s
   }
 }
 
+// The same sum, in the same order, for a small state (small grids, whose
+// whole evaluation is a latency chain): the eight warps of a block load 32
+// slots of 32 consecutive entries per round (four independent coalesced
+// loads per thread; the serial kernel's loads end up interleaved with its
+// additions, ~3 in flight) into shared memory, and warp 0 adds them in slot
+// order -- bitwise equal to reduce_slots_kernel.
+__global__ void __launch_bounds__(256) reduce_slots_staged_kernel(const double2* __restrict__ slots, int Gc,
+                                                                  size_t n, double2* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ double2 val[32][32];  // [slot][entry]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (size_t base = (size_t)blockIdx.x * 32; base < n; base += (size_t)gridDim.x * 32) {
+    const size_t i = base + lane;
+    double2 a = czero();
+    for (int g0 = 0; g0 < Gc; g0 += 32) {
+      double2 r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int g = g0 + w + 8 * k;
+        r[k] = (g < Gc && i < n) ? __ldg(slots + (size_t)g * n + i) : czero();
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) val[w + 8 * k][lane] = r[k];
+      __syncthreads();
+      if (w == 0) {
+        const int ng = min(32, Gc - g0);
+        for (int g = 0; g < ng; ++g) a = (g0 + g == 0) ? val[0][lane] : cadd(a, val[g][lane]);
+      }
+      __syncthreads();
+    }
+    if (w == 0 && i < n) out[i] = a;
+  }
+}
+
 // The same sum for many slots (small grids, whose pass C runs many phase
 // groups): the Gc slots are split into RP contiguous ranges, warp r of a
 // block sums range r for 32 consecutive entries (coalesced), and warp 0 adds
