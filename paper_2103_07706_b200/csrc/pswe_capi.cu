@@ -1168,7 +1168,13 @@ int step_impl_w(pswe_ctx* c, const PhaseSet& ps, double dt, Full3 U, Full3w out,
   const GridDev G = c->grid();
   const Prop pr = c->prop();
   TRY(ensure_hgate(c, ps.P));
-  const int gb = elem_grid(c, (size_t)W * n), gp = elem_grid(c, (size_t)W * c->compact_elems());
+  // stage kernels: per-mode sincos and exponentials, a latency chain at small
+  // sizes -- 64-thread blocks spread few modes over more SMs (64^2: 64 blocks
+  // instead of 16)
+  static const bool wide = getenv("PSWE_STAGE_TB256") != nullptr;  // A/B switch
+  const int tb = (!wide && (size_t)W * n <= (size_t(1) << 15)) ? 64 : 256;
+  const int gb = tb == 256 ? elem_grid(c, (size_t)W * n) : (int)(((size_t)W * n + tb - 1) / tb);
+  const int gp = elem_grid(c, (size_t)W * c->compact_elems());
   // stage 1 (its input packed here; the stage kernels pack the inputs of
   // RHS 2 and 3 themselves, alternating the gate statistic A / B)
   c->pdl = pdl_enabled();
@@ -1176,19 +1182,19 @@ int step_impl_w(pswe_ctx* c, const PhaseSet& ps, double dt, Full3 U, Full3w out,
   c->launches++;
   TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, stage1_kernel, gb, 256, 0, st, G, pr, dt, U, (const double2*)Ac, edt, u1, c->flags.p, W, ws,
+  CU(launch_k(c->pdl, stage1_kernel, gb, tb, 0, st, G, pr, dt, U, (const double2*)Ac, edt, u1, c->flags.p, W, ws,
               hgate_of(c, ps.P, HERM_BIT0, HG_A), PackOut{Uc, c->hgate.p + HG_B}));
   c->launches++;
   // stage 2
   TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, stage2_kernel, gb, 256, 0, st, G, pr, dt, U, f3c(u1), (const double2*)Ac, u2, c->flags.p, W,
+  CU(launch_k(c->pdl, stage2_kernel, gb, tb, 0, st, G, pr, dt, U, f3c(u1), (const double2*)Ac, u2, c->flags.p, W,
               ws, hgate_of(c, ps.P, HERM_BIT0 + 1, HG_B), PackOut{Uc, c->hgate.p + HG_A}));
   c->launches++;
   // stage 3
   TRY(rhs_compact(c, ps, Uc, Ac, st, true));
   c->pdl = pdl_enabled();
-  CU(launch_k(c->pdl, stage3_kernel, gb, 256, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)Ac, out,
+  CU(launch_k(c->pdl, stage3_kernel, gb, tb, 0, st, G, pr, dt, f3c(edt), f3c(u2), (const double2*)Ac, out,
               c->flags.p, W, ws, hgate_of(c, ps.P, HERM_BIT0 + 2, HG_A)));
   c->launches++;
   CU(cudaGetLastError());
