@@ -1,7 +1,7 @@
 """Mid-size points (256^2 / 512^2 at M = 8, 32): total device time per RHS for
 1, 2 and 4 lanes (L2 flushed between calls, as in bench.py) and the per-pass
 split of the one-lane evaluation (profiling events)."""
-import sys
+import os, sys
 sys.path.insert(0, ".")
 import torch
 import paper_2103_07706_b200 as pk
@@ -17,7 +17,7 @@ for r, M in pts:
     Uc = ctx.pack(pk.dynamics.upload(ctx, c.state))
     Ac = ctx.empty_compact()
     line = f"n={c.grid.nx} M={M} P={c.P}:"
-    for lanes in (4, 2, 1):
+    for lanes in map(int, os.environ.get("LANES", "4,2,1").split(",")):
         ctx.set_lanes(lanes)
         for _ in range(3):
             ctx.averaged_tendency_compact(Uc, Ac)
