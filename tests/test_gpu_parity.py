@@ -520,6 +520,46 @@ def test_latency_paths_are_bitwise_identical(tmp_path):
     assert np.array_equal(outs[0][1], outs[1][1])
 
 
+def test_staged_slot_reduction_gives_the_same_bits(tmp_path):
+    """The staged slot reduction (32 slots per load round through shared
+    memory) and the stage kernels' 64-thread blocks on small grids change
+    scheduling only: with both switched off (PSWE_NO_STAGED: the serial
+    batches; PSWE_STAGE_TB256) a fresh process gives the same bits for 64^2
+    evaluations with 15, 63 (two rounds of the cluster kernel's slots) and
+    255 phases, a 32^2 M = 64 evaluation (127 slots: four rounds), a 256^2
+    M = 8 evaluation (three-pass path, staged) and a C2 step."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2103_07706_b200 as pk\n"
+        "from paper_2103_07706_b200 import cases\n"
+        "outs = []\n"
+        "for r, M in ((4, 8), (4, 32), (4, 128), (3, 64), (6, 8)):\n"
+        "    c = cases.case_c5(r, M)\n"
+        "    a = pk.averaged_tendency(c.state, c.quadrature, c.params, pk.PropagatorSpec.exact())\n"
+        "    outs.append(np.concatenate([a.u.ravel(), a.v.ravel(), a.eta.ravel()]))\n"
+        "c = cases.case_c2()\n"
+        "cfg = pk.StepConfig(dt=c.dt, quadrature=c.quadrature, propagator_spec=pk.PropagatorSpec.exact())\n"
+        "s = pk.step_averaged_ssprk3(c.state, cfg, c.params)\n"
+        "outs.append(np.concatenate([s.u.ravel(), s.v.ravel(), s.eta.ravel()]))\n"
+        "np.save(sys.argv[1], np.concatenate(outs))\n" % str(ROOT))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
+    outs = []
+    for i, env in enumerate(({}, {"PSWE_NO_STAGED": "1", "PSWE_STAGE_TB256": "1"})):
+        f = tmp_path / f"r{i}.npy"
+        p = subprocess.run([sys.executable, "-c", code, str(f)], env={**base, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        outs.append(np.load(f))
+    assert np.all(np.isfinite(outs[0]))
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_pairs_per_cta_give_the_same_bits(tmp_path):
     """Pass B's CTAs may take two phase pairs each (chosen for grids of many
     waves); scheduling only: one and two pairs per CTA give the same bits at
