@@ -69,8 +69,7 @@ template <int N, int C, bool MW>
 __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
     cfused_kernel(GridDev G, Prop pr, PhaseDev ph, int Gc, const double2* __restrict__ Uc,
                   const double2* __restrict__ ctab, double2* __restrict__ out, double* __restrict__ pscale) {
-  griddep_wait();
-  griddep_launch();
+  // the dependency wait is below, after the part that reads nothing the kernels before this one wrote
   using W = CFusedW<N, C>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, Ky = W::Ky, Kx = W::Kx, KyKx = W::KyKx, LD = W::LD;
   constexpr int JL = W::JL, NT = W::NT;
@@ -115,6 +114,10 @@ __global__ void __launch_bounds__(CFusedW<N, C>::NT, 1)
   const WLane wlx = wlane<N>(G.twx, t), wly = wlane<N>(G.twy, t);
   for (int i = threadIdx.x; i < Ky; i += NT) kys[i] = G.kyc[i];
   for (int i = threadIdx.x; i < Kx; i += NT) kxs[i] = G.kxc[i];
+  griddep_wait();  // Uc, the gate scale and the slots belong to the kernels before this one
+  // only now: the next kernel (a stage kernel when the slot reduction is skipped) reads states written
+  // two kernels back before its own wait, so it must not start until this kernel has waited
+  griddep_launch();
   const int nmode = jl_n * Kx;  // my compact modes
   constexpr int MI = W::MI;
   // one window: my modes' U and b stay in shared memory for all phases

@@ -95,8 +95,7 @@ template <int N, bool MW>
 __global__ void __launch_bounds__(FusedW<N>::NT)
     fused_kernel(GridDev G, Prop pr, PhaseDev ph, int Gc, const double2* __restrict__ Uc,
                  const double2* __restrict__ ctab, double2* __restrict__ out, double* __restrict__ pscale) {
-  griddep_wait();
-  griddep_launch();
+  // the dependency wait is below, after the part that reads nothing the kernels before this one wrote
   using W = FusedW<N>;
   constexpr int T = W::T, P = W::P, GPW = W::GPW, Ky = W::Ky, Kx = W::Kx, KyKx = W::KyKx, LD = W::LD;
   constexpr int CPT = W::CPT, NT = W::NT;
@@ -124,6 +123,10 @@ __global__ void __launch_bounds__(FusedW<N>::NT)
     for (int idx = threadIdx.x; idx < 3 * KyKx; idx += NT) slot[idx] = add ? cadd(slot[idx], ACC[idx]) : ACC[idx];
   };
   zero_acc();
+  griddep_wait();  // Uc, the gate scale and the slots belong to the kernels before this one
+  // only now: the next kernel (a stage kernel when the slot reduction is skipped) reads states written
+  // two kernels back before its own wait, so it must not start until this kernel has waited
+  griddep_launch();
   int wcur = MW && lo < hi ? ph.win[lo] : 0;
 
 #pragma unroll 1

@@ -1434,41 +1434,64 @@ __device__ __forceinline__ void pack_stats_flush(const PackOut& po, double (&dma
 __device__ __forceinline__ int mirror_ix(const GridDev& G, int ix) { return (G.nx - ix) % G.nx; }
 __device__ __forceinline__ int mirror_jy(const GridDev& G, int jy) { return (G.ny - jy) % G.ny; }
 
+// The stage kernels start under programmatic dependent launch while the
+// RHS's last kernel (the slot reduction) still runs: everything that does
+// not depend on that RHS -- the loads of the step's states and the
+// exponentials applied to them -- is done before the wait, only the part that
+// reads the tendency Ac after it (small grids, where a stage kernel is one
+// latency chain per thread: ~1 us of that chain moves under the reduction).
+// stage_wait: once per thread, at block-uniform points only.
+__device__ __forceinline__ void stage_wait(bool& waited, const HermGate& hg) {
+  if (waited) return;
+  griddep_wait();
+  waited = true;
+  if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
+}
+
 // stage 1 (integrator.py:96-98): e_dt = E(dt) U;  u1 = e_dt + dt * E(dt) A(U)
 __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const double2* __restrict__ Ac,
                               Full3w edt, Full3w u1, int* flags, int W, size_t ws,
                               HermGate hg, PackOut po) {
-  griddep_wait();
   griddep_launch();
-  if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
+  bool waited = false;
   const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   double dmax[3] = {0.0, 0.0, 0.0};
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
     const size_t t = i0 + threadIdx.x;
-    C3 o = c3zero();
-    if (t < N) {
-      const size_t win = t / n, i = t - win * n;
-      const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
-      const double kx = G.kxf[ix], ky = G.kyf[jy];
+    C3 o = c3zero(), e = c3zero(), em = c3zero();
+    size_t win = 0, i = 0;
+    int ix = 0, jy = 0, j = 0, r = 0, mx = 0, my = 0;
+    double kx = 0.0, ky = 0.0, kxm = 0.0, kym = 0.0;
+    double2 cd = czero();
+    bool pk = false;
+    if (t < N) {  // before the wait: E(dt) U at this mode and, for a packed mode, at its mirror
+      win = t / n, i = t - win * n;
+      ix = (int)(i / G.ny), jy = (int)(i % G.ny);
+      kx = G.kxf[ix], ky = G.kyf[jy];
       const Full3 Uw = wshift(U, win * ws);
-      const double2 cd = pr.kind == 0 ? c12_of(G.ph, kx, ky, dt) : czero();  // this mode and its mirror
-      const C3 e = expLc(cd, dt, ld3(Uw, i), G.ph, kx, ky, pr);
+      cd = pr.kind == 0 ? c12_of(G.ph, kx, ky, dt) : czero();  // this mode and its mirror
+      e = expLc(cd, dt, ld3(Uw, i), G.ph, kx, ky, pr);
+      pk = po.Uc && packed_mode(G, ix, jy, j, r);
+      if (pk) {
+        mx = mirror_ix(G, ix), my = mirror_jy(G, jy);
+        kxm = G.kxf[mx], kym = G.kyf[my];
+        em = expLc(cd, dt, ld3(Uw, (size_t)mx * G.ny + my), G.ph, kxm, kym, pr);
+      }
+    }
+    stage_wait(waited, hg);
+    if (t < N) {
       const C3 ea = expLc(cd, dt, compact_at(G, Ac + win * cs, ix, jy), G.ph, kx, ky, pr);
       o = c3add(e, c3scale(dt, ea));
       st3(wshift(edt, win * ws), i, e);
       st3(wshift(u1, win * ws), i, o);
-      int j, r;
-      if (po.Uc && packed_mode(G, ix, jy, j, r)) {  // u1 at -k too: the packed input of RHS 2
-        const int mx = mirror_ix(G, ix), my = mirror_jy(G, jy);
-        const size_t im = (size_t)mx * G.ny + my;
-        const double kxm = G.kxf[mx], kym = G.kyf[my];
-        const C3 om = c3add(expLc(cd, dt, ld3(Uw, im), G.ph, kxm, kym, pr),
-                            c3scale(dt, expLc(cd, dt, compact_at(G, Ac + win * cs, mx, my), G.ph, kxm, kym, pr)));
+      if (pk) {  // u1 at -k too: the packed input of RHS 2
+        const C3 om = c3add(em, c3scale(dt, expLc(cd, dt, compact_at(G, Ac + win * cs, mx, my), G.ph, kxm, kym, pr)));
         pack_store(G, po, win * cs, j, r, o, om, dmax);
       }
     }
     flag_nonfinite(o, 1, flags);
   }
+  stage_wait(waited, hg);
   if (po.Uc) pack_stats_flush(po, dmax);
 }
 
@@ -1476,39 +1499,52 @@ __global__ void stage1_kernel(GridDev G, Prop pr, double dt, Full3 U, const doub
 __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, const double2* __restrict__ Ac,
                               Full3w u2, int* flags, int W, size_t ws,
                               HermGate hg, PackOut po) {
-  griddep_wait();
   griddep_launch();
-  if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
+  bool waited = false;
   const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   const double h = 0.5 * dt;
   double dmax[3] = {0.0, 0.0, 0.0};
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
     const size_t t = i0 + threadIdx.x;
-    C3 o = c3zero();
-    if (t < N) {
-      const size_t win = t / n, i = t - win * n;
-      const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
-      const double kx = G.kxf[ix], ky = G.kyf[jy];
+    C3 o = c3zero(), a = c3zero(), am = c3zero(), y1 = c3zero(), y1m = c3zero();
+    size_t win = 0, i = 0;
+    int ix = 0, jy = 0, j = 0, r = 0, mx = 0, my = 0;
+    double kx = 0.0, ky = 0.0, kxm = 0.0, kym = 0.0;
+    double2 cm = czero();
+    bool pk = false;
+    if (t < N) {  // before the wait: E(dt/2) U and the load of u1, at this mode and its mirror
+      win = t / n, i = t - win * n;
+      ix = (int)(i / G.ny), jy = (int)(i % G.ny);
+      kx = G.kxf[ix], ky = G.kyf[jy];
       const Full3 Uw = wshift(U, win * ws), u1w = wshift(u1, win * ws);
-      const double2 ch = pr.kind == 0 ? c12_of(G.ph, kx, ky, h) : czero(), cm = cmk(-ch.x, ch.y);  // +-dt/2
-      const C3 a = expLc(ch, h, ld3(Uw, i), G.ph, kx, ky, pr);
-      const C3 y = c3add(ld3(u1w, i), c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
+      const double2 ch = pr.kind == 0 ? c12_of(G.ph, kx, ky, h) : czero();
+      cm = cmk(-ch.x, ch.y);  // +-dt/2
+      a = expLc(ch, h, ld3(Uw, i), G.ph, kx, ky, pr);
+      y1 = ld3(u1w, i);
+      pk = po.Uc && packed_mode(G, ix, jy, j, r);
+      if (pk) {
+        mx = mirror_ix(G, ix), my = mirror_jy(G, jy);
+        const size_t im = (size_t)mx * G.ny + my;
+        kxm = G.kxf[mx], kym = G.kyf[my];
+        am = expLc(ch, h, ld3(Uw, im), G.ph, kxm, kym, pr);
+        y1m = ld3(u1w, im);
+      }
+    }
+    stage_wait(waited, hg);
+    if (t < N) {
+      const C3 y = c3add(y1, c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
       const C3 b = expLc(cm, -h, y, G.ph, kx, ky, pr);
       o = c3add(c3scale(0.75, a), c3scale(0.25, b));
       st3(wshift(u2, win * ws), i, o);
-      int j, r;
-      if (po.Uc && packed_mode(G, ix, jy, j, r)) {  // u2 at -k too: the packed input of RHS 3
-        const int mx = mirror_ix(G, ix), my = mirror_jy(G, jy);
-        const size_t im = (size_t)mx * G.ny + my;
-        const double kxm = G.kxf[mx], kym = G.kyf[my];
-        const C3 am = expLc(ch, h, ld3(Uw, im), G.ph, kxm, kym, pr);
-        const C3 ym = c3add(ld3(u1w, im), c3scale(dt, compact_at(G, Ac + win * cs, mx, my)));
+      if (pk) {  // u2 at -k too: the packed input of RHS 3
+        const C3 ym = c3add(y1m, c3scale(dt, compact_at(G, Ac + win * cs, mx, my)));
         const C3 om = c3add(c3scale(0.75, am), c3scale(0.25, expLc(cm, -h, ym, G.ph, kxm, kym, pr)));
         pack_store(G, po, win * cs, j, r, o, om, dmax);
       }
     }
     flag_nonfinite(o, 2, flags);
   }
+  stage_wait(waited, hg);
   if (po.Uc) pack_stats_flush(po, dmax);
 }
 
@@ -1516,25 +1552,33 @@ __global__ void stage2_kernel(GridDev G, Prop pr, double dt, Full3 U, Full3 u1, 
 __global__ void stage3_kernel(GridDev G, Prop pr, double dt, Full3 edt, Full3 u2, const double2* __restrict__ Ac,
                               Full3w out, int* flags, int W, size_t ws,
                               HermGate hg) {
-  griddep_wait();
   griddep_launch();
-  if (hg.bit >= 0 && blockIdx.x == 0) herm_eval_block(hg);
+  bool waited = false;
   const size_t n = (size_t)G.nx * G.ny, N = (size_t)W * n, cs = 3 * (size_t)G.Ky * G.Kx;
   const double h = 0.5 * dt;
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x; i0 < N; i0 += (size_t)gridDim.x * blockDim.x) {
     const size_t t = i0 + threadIdx.x;
-    C3 o = c3zero();
+    C3 o = c3zero(), y2 = c3zero(), ed = c3zero();
+    size_t win = 0, i = 0;
+    int ix = 0, jy = 0;
+    double kx = 0.0, ky = 0.0;
+    if (t < N) {  // before the wait: the loads of u2 and e_dt
+      win = t / n, i = t - win * n;
+      ix = (int)(i / G.ny), jy = (int)(i % G.ny);
+      kx = G.kxf[ix], ky = G.kyf[jy];
+      y2 = ld3(wshift(u2, win * ws), i);
+      ed = ld3(wshift(edt, win * ws), i);
+    }
+    stage_wait(waited, hg);
     if (t < N) {
-      const size_t win = t / n, i = t - win * n;
-      const int ix = (int)(i / G.ny), jy = (int)(i % G.ny);
-      const double kx = G.kxf[ix], ky = G.kyf[jy];
-      const C3 y = c3add(ld3(wshift(u2, win * ws), i), c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
+      const C3 y = c3add(y2, c3scale(dt, compact_at(G, Ac + win * cs, ix, jy)));
       const C3 b = expL(h, y, G.ph, kx, ky, pr);
-      o = c3add(c3scale(1.0 / 3.0, ld3(wshift(edt, win * ws), i)), c3scale(2.0 / 3.0, b));
+      o = c3add(c3scale(1.0 / 3.0, ed), c3scale(2.0 / 3.0, b));
       st3(wshift(out, win * ws), i, o);
     }
     flag_nonfinite(o, 3, flags);
   }
+  stage_wait(waited, hg);
 }
 
 // phase table (c1, c2)[p][j][r] of the exact exponential for every live phase
