@@ -520,6 +520,46 @@ def test_latency_paths_are_bitwise_identical(tmp_path):
     assert np.array_equal(outs[0][1], outs[1][1])
 
 
+def test_prewait_work_of_the_step_chain_is_race_free(tmp_path):
+    """Under programmatic dependent launch the one-launch small-grid kernels
+    and the stage kernels do their chain-independent work before the
+    dependency wait ("Dependent-launch prologues").  That is only
+    legal while no kernel starts before everything two kernels back has
+    completed; the shortest chains test it: a single-node (T = 0) run, where a
+    stage kernel directly follows the one-launch kernel (no slot reduction in
+    between), at 64^2 and 32^2, and a C2 run.  With dependent launch
+    switched off (fresh process) the bits must be the same."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2103_07706_b200 as pk\n"
+        "from paper_2103_07706_b200 import cases\n"
+        "res = []\n"
+        "for c, dt, n, quad in ((cases.case_c2(), 180.0, 96, pk.kernel_weights(0.0, 0)),\n"
+        "                       (cases.case_c5(3, 8), 180.0, 96, pk.kernel_weights(0.0, 0)),\n"
+        "                       (cases.case_c2(), None, 12, None)):\n"
+        "    cfg = pk.StepConfig(dt=dt or c.dt, quadrature=quad or c.quadrature,\n"
+        "                        propagator_spec=pk.PropagatorSpec.exact())\n"
+        "    s = pk.run(c.state, cfg, c.params, t_end=n * cfg.dt).states[-1]\n"
+        "    res += [s.u.ravel(), s.v.ravel(), s.eta.ravel()]\n"
+        "np.save(sys.argv[1], np.concatenate(res))\n" % str(ROOT))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
+    outs = []
+    for i, env in enumerate(({}, {"PSWE_NO_PDL": "1"})):
+        f = tmp_path / f"r{i}.npy"
+        p = subprocess.run([sys.executable, "-c", code, str(f)], env={**base, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        outs.append(np.load(f))
+    assert np.all(np.isfinite(outs[0]))
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_staged_slot_reduction_gives_the_same_bits(tmp_path):
     """The staged slot reduction (32 slots per load round through shared
     memory) and the stage kernels' 64-thread blocks on small grids change
