@@ -527,8 +527,10 @@ def test_prewait_work_of_the_step_chain_is_race_free(tmp_path):
     legal while no kernel starts before everything two kernels back has
     completed; the shortest chains test it: a single-node (T = 0) run, where a
     stage kernel directly follows the one-launch kernel (no slot reduction in
-    between), at 64^2 and 32^2, and a C2 run.  With dependent launch
-    switched off (fresh process) the bits must be the same."""
+    between), at 64^2 and 32^2, a C2 run, and a 700-step single-node run
+    (eight steps per graph, no copies between them).  With dependent launch
+    and the eight-step graphs switched off (fresh process) the bits must be
+    the same."""
     import os
     import subprocess
     import sys
@@ -541,16 +543,20 @@ def test_prewait_work_of_the_step_chain_is_race_free(tmp_path):
         "from paper_2103_07706_b200 import cases\n"
         "res = []\n"
         "for c, dt, n, quad in ((cases.case_c2(), 180.0, 96, pk.kernel_weights(0.0, 0)),\n"
-        "                       (cases.case_c5(3, 8), 180.0, 96, pk.kernel_weights(0.0, 0)),\n"
+        "                       (cases.case_c1(), 180.0, 96, pk.kernel_weights(0.0, 0)),\n"
         "                       (cases.case_c2(), None, 12, None)):\n"
         "    cfg = pk.StepConfig(dt=dt or c.dt, quadrature=quad or c.quadrature,\n"
         "                        propagator_spec=pk.PropagatorSpec.exact())\n"
         "    s = pk.run(c.state, cfg, c.params, t_end=n * cfg.dt).states[-1]\n"
         "    res += [s.u.ravel(), s.v.ravel(), s.eta.ravel()]\n"
+        "c = cases.case_c2()  # long enough for the eight-step graphs (pswe_run)\n"
+        "cfg = pk.StepConfig(dt=180.0, quadrature=pk.kernel_weights(0.0, 0), propagator_spec=pk.PropagatorSpec.exact())\n"
+        "s = pk.run(c.state, cfg, c.params, t_end=700 * cfg.dt).states[-1]\n"
+        "res += [s.u.ravel(), s.v.ravel(), s.eta.ravel()]\n"
         "np.save(sys.argv[1], np.concatenate(res))\n" % str(ROOT))
     base = {k: v for k, v in os.environ.items() if not k.startswith("PSWE_")}
     outs = []
-    for i, env in enumerate(({}, {"PSWE_NO_PDL": "1"})):
+    for i, env in enumerate(({}, {"PSWE_NO_PDL": "1", "PSWE_NO_MULTISTEP_GRAPH": "1"})):
         f = tmp_path / f"r{i}.npy"
         p = subprocess.run([sys.executable, "-c", code, str(f)], env={**base, **env},
                            capture_output=True, text=True, timeout=300)
